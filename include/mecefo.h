@@ -1,0 +1,222 @@
+/*
+ * mecefo.h — C-ABI of the B200-native MeCeFO degraded-step engine.
+ *
+ * Drop-in boundary for the step / failure-handling path of the reference CPU
+ * simulator `faultsim` (pkg/src/faultsim, arXiv 2510.16415). The reference is
+ * pure Python over float64 numpy arrays; its "FFI" is the module-level
+ * function surface that `faultsim.harness` dispatches through by attribute
+ * lookup (harness.py:209-249). Each entry point below names the reference
+ * function it replaces (file:line under pkg/src/faultsim/).
+ *
+ * Conventions
+ *  - All tensor arguments are caller-owned DEVICE pointers (e.g. PyTorch
+ *    allocations), row-major, plus sizes and a cudaStream_t passed as void*.
+ *    Nothing here allocates device memory except mecefo_engine_create (a small
+ *    RoPE table); scratch space comes from a caller-provided workspace.
+ *  - Activations that feed GEMMs are in the engine's compute precision
+ *    (MECEFO_PREC_BF16 -> tcgen05 tensor cores, MECEFO_PREC_F32 -> fp32 FFMA
+ *    path for the 1e-4 parity mode). Master weights, the residual stream,
+ *    gradients and optimizer state are fp32.
+ *  - Gradient outputs ACCUMULATE: g += alpha * dL/dW. alpha carries the
+ *    Eq. (1) 1/|N_{l,#}| factor (cluster.py:292-322); a rank outside an active
+ *    set simply passes NULL for that gradient (select, never multiply, so a
+ *    non-finite value on an excluded rank cannot leak).
+ *  - Every call is stream-ordered and asynchronous; no host synchronisation.
+ *  - Return value: MECEFO_OK or an error code mirroring the reference's
+ *    exception classes (errors.py:8-33); mecefo_last_error() gives the text.
+ */
+#ifndef MECEFO_H
+#define MECEFO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MECEFO_OK = 0,
+  MECEFO_ERR_CONTRACT = 1,      /* errors.py:12 ContractViolation */
+  MECEFO_ERR_NUMERICAL = 2,     /* errors.py:16 NumericalFailure */
+  MECEFO_ERR_SVD_NOCONV = 3,    /* errors.py:20 SvdConvergenceError */
+  MECEFO_ERR_UNRECOVERABLE = 4, /* errors.py:28 UnrecoverableRankError */
+  MECEFO_ERR_CONSISTENCY = 5,   /* errors.py:32 ConsistencyError */
+  MECEFO_ERR_CONFIG = 6,        /* errors.py:8 ConfigError */
+  MECEFO_ERR_CUDA = 7           /* CUDA runtime failure (no reference analogue) */
+};
+
+enum { MECEFO_PREC_F32 = 0, MECEFO_PREC_BF16 = 1 };
+
+/* model.py:30-31 CACHE_FULL / CACHE_FFN_INPUT_ONLY */
+enum { MECEFO_CACHE_FULL = 0, MECEFO_CACHE_FFN_INPUT_ONLY = 1 };
+
+/* model.py:40-61 ModelConfig (+ the engine's compute precision). */
+typedef struct {
+  int64_t vocab, hidden, heads, ffn, layers, seq_len;
+  int32_t rope;
+  int32_t precision;
+} mecefo_dims;
+
+typedef struct mecefo_engine mecefo_engine;
+
+/* model.py:64-90 LayerWeights, in the engine's HBM layout: q,k,v stacked as
+ * one (3m, m) matrix and gate,up stacked as one (2f, m) matrix — exactly the
+ * canonical parameter order of model.py:35, so a flat parameter buffer in
+ * that order provides these views without copies. *_c are the operand copies
+ * in compute precision (the masters themselves in fp32 mode). */
+typedef struct {
+  const float* w_qkv;
+  const float* w_o;
+  const float* norm_mha;
+  const float* w_gu;
+  const float* w_down;
+  const float* norm_ffn;
+  const void* w_qkv_c;
+  const void* w_o_c;
+  const void* w_gu_c;
+  const void* w_down_c;
+} mecefo_layer_weights;
+
+/* model.py:376-381 BlockCache. x and x1 (fp32, (tokens, hidden)) are the
+ * whole lean cache; the remaining fields are used only by CACHE_FULL. */
+typedef struct {
+  float* x;
+  float* x1;
+  void* h1;
+  float* inv1;
+  void* qkv;
+  void* ctx;
+  float* lse;
+  void* h2;
+  float* inv2;
+  void* gu;
+  void* act;
+} mecefo_block_cache;
+
+/* Per-layer gradient accumulators (fp32, canonical shapes); NULL = skip. */
+typedef struct {
+  float* qkv;      /* (3m, m): q, k, v */
+  float* o;        /* (m, m) */
+  float* norm_mha; /* (m) */
+  float alpha_mha;
+  float* gu;       /* (2f, m): gate, up */
+  float* down;     /* (m, f) */
+  float* norm_ffn; /* (m) */
+  float alpha_ffn;
+} mecefo_layer_grads;
+
+/* approx.py:45-63 ProjectionCache.basis, per kind in FFN_KINDS order
+ * (gate, up, down): V1 (in, rank_pad) and its transpose (rank_pad, in) in
+ * compute precision, zero beyond rank[k] = min(r, in) (approx.py:79). */
+typedef struct {
+  int32_t rank[3];
+  int32_t rank_pad;
+  const void* v1[3];
+  const void* v1t[3];
+} mecefo_projection;
+
+/* AdamW segment: one named parameter of the flat buffer (optim.py:75-93). */
+typedef struct {
+  int64_t offset;
+  int64_t numel;
+  float step_size; /* lr / (1 - beta1^t) */
+  float inv_bc2;   /* 1 / (1 - beta2^t) */
+  float lr_wd;     /* lr * weight_decay */
+  int32_t pad;
+} mecefo_adam_segment;
+
+const char* mecefo_last_error(void);
+const char* mecefo_version(void);
+
+int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims);
+int mecefo_engine_destroy(mecefo_engine* e);
+/* Workspace bytes needed by any call below at `tokens` rows and padded rank. */
+size_t mecefo_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t rank_pad);
+
+/* model.py:398-418 forward_block. Reads cache->x, writes cache->x1, y and
+ * (mode == FULL) the full-cache fields. y may alias the next block's x. */
+int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* cache, float* y,
+                         void* y_c, int64_t tokens, int32_t mode, void* ws, size_t ws_bytes, void* stream);
+
+/* approx.py:99-134 backward_block_neighbor: skip the MHA backward, recompute
+ * the FFN from x1, FFN Wgrads low-rank through `proj` (NULL = exact Wgrads,
+ * the proj=None branch), dx = dy + dx1_ffn. dy_c: optional compute-precision
+ * copy of dy; dx_c: optional compute-precision copy of dx (next GEMM). */
+int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights* lw,
+                                   const mecefo_block_cache* cache, const float* dy, const void* dy_c, float* dx,
+                                   void* dx_c, const mecefo_layer_grads* grads, const mecefo_projection* proj,
+                                   int64_t tokens, void* ws, size_t ws_bytes, void* stream);
+
+/* model.py:421-437 backward_block_exact (requires a FULL cache). */
+int mecefo_backward_block_exact(mecefo_engine* e, const mecefo_layer_weights* lw, const mecefo_block_cache* cache,
+                                const float* dy, const void* dy_c, float* dx, void* dx_c,
+                                const mecefo_layer_grads* grads, int64_t tokens, void* ws, size_t ws_bytes,
+                                void* stream);
+
+/* model.py:207-225 ffn_forward == approx.py:90-96 recompute_ffn. Outputs in
+ * compute precision (h2, gate, up, act, down) and fp32 inv_rms2; any output
+ * pointer may be NULL except those needed downstream. */
+int mecefo_recompute_ffn(mecefo_engine* e, const mecefo_layer_weights* lw, const float* x1, int64_t tokens,
+                         void* h2, float* inv_rms2, void* gate, void* up, void* act, float* down, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* approx.py:24-42 lowrank_wgrad(g_y (out,b), x (in,b), v1 (in,r)) ->
+ * (out, in) = g_y (x^T v1) v1^T, all operands in compute precision, out fp32
+ * (out += alpha * result). */
+int mecefo_lowrank_wgrad(mecefo_engine* e, const void* g_y, const void* x, const void* v1, float* out,
+                         int64_t n_out, int64_t n_in, int64_t batch, int64_t rank, float alpha, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* model.py:463 embedding gather: x[t] = embedding[tokens[t]]. */
+int mecefo_embedding_forward(mecefo_engine* e, const int64_t* tokens, const float* embedding, float* x,
+                             int64_t n_tokens, void* stream);
+
+/* model.py:469-471 + 492-509: xf = rmsnorm(x_last) * final_norm; logits =
+ * xf unembedding^T; mean CE -> loss[0]; dlogits = (softmax-onehot)/n written
+ * in place over `logits` (compute precision, (tokens, vocab)). */
+int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
+                             const int64_t* targets, int64_t tokens, void* xf, float* inv_f, void* logits,
+                             float* loss, void* ws, size_t ws_bytes, void* stream);
+
+/* model.py:476-483 head_backward (+ accumulate into g_final_norm/g_unemb). */
+int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* final_norm, const float* inv_f,
+                         const void* xf, const void* dlogits, const void* unemb_c, float* dx, void* dx_c,
+                         float* g_final_norm, float* g_unemb, float alpha, int64_t tokens, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* model.py:486-489 embedding_backward: g[tokens[t]] += alpha * dx0[t]. */
+int mecefo_embedding_backward(mecefo_engine* e, const int64_t* tokens, const float* dx0, float* g_emb,
+                              float alpha, int64_t n_tokens, void* stream);
+
+/* cluster.py:292-322 Eq. (1) helper on a flat fp32 range: out = beta*out + alpha*src. */
+int mecefo_scale_accumulate(const float* src, float* out, int64_t n, float alpha, float beta, void* stream);
+
+/* fp32 -> compute-precision copy (weights' operand shadows). */
+int mecefo_cast(mecefo_engine* e, const float* src, void* dst, int64_t n, void* stream);
+
+/* optim.py:55-57 _check_grad as a device flag: flag[0] |= any(!isfinite(v)). */
+int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream);
+
+/* optim.py:96-103 apply_step with AdamW (optim.py:75-93) over a flat buffer;
+ * skipped parameters are omitted from `segs`. `segs` is a DEVICE array.
+ * shadow (optional) receives the updated weights in compute precision. */
+int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t nseg, int64_t max_numel, float* w,
+                      const float* grad, float* m, float* v, void* shadow, float beta1, float beta2, float eps,
+                      void* stream);
+
+/* Generic C[M,N] (+)= alpha * A B^T on the engine's GEMM path (used by the
+ * projection refresh, linalg.py:97-142). a_kmajor: A(i,k) at a[i*lda+k],
+ * else a[k*lda+i]; likewise B(n,k). C fp32 (ldc), beta in {0,1}. */
+int mecefo_gemm(mecefo_engine* e, int64_t M, int64_t N, int64_t K, const void* a, int64_t lda, int32_t a_kmajor,
+                const void* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha, float beta,
+                void* stream);
+
+/* Number of kernels this library has launched (evidence counter). */
+int64_t mecefo_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MECEFO_H */

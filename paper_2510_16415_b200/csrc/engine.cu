@@ -1,0 +1,884 @@
+// Host side of the MeCeFO engine: GEMM dispatch (tcgen05 bf16 / fp32 SIMT),
+// TMA descriptor cache, block-level orchestration of the lean and exact
+// steps, and the C-ABI declared in include/mecefo.h.
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/mecefo.h"
+#include "attention.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+using namespace mecefo;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t _e = (expr);                                                                    \
+    if (_e != cudaSuccess)                                                                      \
+      return set_err(MECEFO_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                     __FILE__, __LINE__);                                                       \
+  } while (0)
+
+#define TRY(expr)               \
+  do {                          \
+    int _rc = (expr);           \
+    if (_rc != MECEFO_OK) return _rc; \
+  } while (0)
+
+int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(MECEFO_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+  return MECEFO_OK;
+}
+
+// Bump allocator over the caller's workspace.
+struct Ws {
+  uint8_t* base;
+  size_t cap, used = 0;
+  Ws(void* p, size_t c) : base(reinterpret_cast<uint8_t*>(p)), cap(c) {}
+  int take(size_t bytes, void** out) {
+    size_t off = (used + 255) & ~size_t(255);
+    if (off + bytes > cap)
+      return set_err(MECEFO_ERR_CONTRACT, "workspace too small: need %zu more bytes (cap %zu)", off + bytes - cap,
+                     cap);
+    *out = base + off;
+    used = off + bytes;
+    return MECEFO_OK;
+  }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct TmKey {
+  const void* p;
+  int64_t inner, outer, ld;
+  int box0, box1;
+  bool operator==(const TmKey& o) const {
+    return p == o.p && inner == o.inner && outer == o.outer && ld == o.ld && box0 == o.box0 && box1 == o.box1;
+  }
+};
+struct TmHash {
+  size_t operator()(const TmKey& k) const {
+    size_t h = std::hash<const void*>()(k.p);
+    auto mix = [&](int64_t v) { h ^= std::hash<int64_t>()(v) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2); };
+    mix(k.inner); mix(k.outer); mix(k.ld); mix(k.box0); mix(k.box1);
+    return h;
+  }
+};
+
+}  // namespace
+
+struct mecefo_engine {
+  mecefo_dims d;
+  int prec;
+  int ps;  // bytes per compute-precision element
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  std::mutex mu;
+  std::unordered_map<TmKey, CUtensorMap, TmHash> tmaps;
+};
+
+namespace {
+
+int make_tmap(mecefo_engine* e, CUtensorMap* out, const void* p, int64_t inner, int64_t outer, int64_t ld, int box0,
+              int box1) {
+  TmKey key{p, inner, outer, ld, box0, box1};
+  {
+    std::lock_guard<std::mutex> lk(e->mu);
+    auto it = e->tmaps.find(key);
+    if (it != e->tmaps.end()) { *out = it->second; return MECEFO_OK; }
+  }
+  auto enc = get_encode();
+  if (!enc) return set_err(MECEFO_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  if ((reinterpret_cast<uintptr_t>(p) & 15) != 0)
+    return set_err(MECEFO_ERR_CONTRACT, "bf16 GEMM operand %p is not 16-byte aligned", p);
+  if ((ld * 2) % 16 != 0)
+    return set_err(MECEFO_ERR_CONTRACT, "bf16 GEMM operand leading dimension %lld not a multiple of 8 elements",
+                   (long long)ld);
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(MECEFO_ERR_CONTRACT, "cuTensorMapEncodeTiled failed (%d) for %lldx%lld ld %lld box %dx%d", (int)r,
+                   (long long)inner, (long long)outer, (long long)ld, box0, box1);
+  std::lock_guard<std::mutex> lk(e->mu);
+  if (e->tmaps.size() > 4096) e->tmaps.clear();
+  e->tmaps[key] = *out;
+  return MECEFO_OK;
+}
+
+struct Op {
+  const void* p;
+  int64_t ld;
+  bool km;
+};
+
+struct GemmCall {
+  int64_t M = 0, N = 0, K = 0;
+  Op a{}, b{};
+  bool paired = false;
+  int64_t pair_off = 0;
+  Epilogue epi{};
+  int split = 1;
+};
+
+Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, float beta = 0.f,
+                   const float* residual = nullptr, int64_t ldr = 0) {
+  Epilogue e{};
+  e.kind = EPI_STORE;
+  e.out = out; e.ldo = ldo; e.out_prec = out_prec; e.alpha = alpha; e.beta = beta;
+  e.residual = residual; e.ldr = ldr;
+  return e;
+}
+
+template <int BN, bool AK, bool BKM>
+int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
+  using C = TcCfg<BN>;
+  CUtensorMap ta, tb;
+  if (AK) TRY(make_tmap(e, &ta, g.a.p, g.K, g.M, g.a.ld, 64, TC_BM));
+  else TRY(make_tmap(e, &ta, g.a.p, g.M, g.K, g.a.ld, 64, 64));
+  const int64_t rowsB = g.paired ? g.pair_off + g.N : g.N;
+  if (BKM) TRY(make_tmap(e, &tb, g.b.p, g.K, rowsB, g.b.ld, 64, g.paired ? BN / 2 : BN));
+  else TRY(make_tmap(e, &tb, g.b.p, rowsB, g.K, g.b.ld, 64, 64));
+  GemmDev p{};
+  p.M = (int)g.M; p.N = (int)g.N; p.K = (int)g.K;
+  p.paired = g.paired ? 1 : 0;
+  p.pair_off = g.pair_off;
+  p.kblocks = (int)((g.K + TC_BK - 1) / TC_BK);
+  int split = std::max(1, std::min(g.split, p.kblocks));
+  p.kb_per_split = (p.kblocks + split - 1) / split;
+  p.split = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  p.tiles_m = (int)((g.M + TC_BM - 1) / TC_BM);
+  const int cols_per_tile = g.paired ? BN / 2 : BN;
+  p.tiles_n = (int)((g.N + cols_per_tile - 1) / cols_per_tile);
+  p.num_tiles = p.tiles_m * p.tiles_n * p.split;
+  p.epi = g.epi;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<BN, AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int grid = std::min(p.num_tiles, kNumSMs);
+  gemm_tc_kernel<BN, AK, BKM><<<grid, TC_THREADS, C::SMEM, s>>>(ta, tb, p);
+  return check_launch("gemm_tc_kernel");
+}
+
+template <int BN>
+int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
+  if (g.a.km && g.b.km) return launch_tc<BN, true, true>(e, g, s);
+  if (g.a.km && !g.b.km) return launch_tc<BN, true, false>(e, g, s);
+  if (!g.a.km && g.b.km) return launch_tc<BN, false, true>(e, g, s);
+  return launch_tc<BN, false, false>(e, g, s);
+}
+
+int tiles_for(const GemmCall& g, int prec) {
+  if (prec == PREC_BF16) {
+    const int64_t nacc = g.paired ? 2 * g.N : g.N;
+    const int BN = nacc >= 256 ? 256 : (nacc > 64 ? 128 : 64);
+    const int64_t cpt = g.paired ? BN / 2 : BN;
+    return (int)(((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt));
+  }
+  const int64_t cpt = g.paired ? 32 : 64;
+  return (int)(((g.M + 63) / 64) * ((g.N + cpt - 1) / cpt));
+}
+
+int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return MECEFO_OK;
+  if (g.split > 1 && g.epi.kind != EPI_ATOMIC)
+    return set_err(MECEFO_ERR_CONSISTENCY, "split-K requires the atomic epilogue");
+  if (e->prec == PREC_BF16) {
+    if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
+    const int64_t nacc = g.paired ? 2 * g.N : g.N;
+    if (nacc >= 256) return dispatch_tc_major<256>(e, g, s);
+    if (nacc > 64) return dispatch_tc_major<128>(e, g, s);
+    return dispatch_tc_major<64>(e, g, s);
+  }
+  GemmDev p{};
+  p.M = (int)g.M; p.N = (int)g.N; p.K = (int)g.K;
+  p.paired = g.paired ? 1 : 0;
+  p.pair_off = g.pair_off;
+  p.kblocks = (int)((g.K + 15) / 16);
+  int split = std::max(1, std::min(g.split, p.kblocks));
+  p.kb_per_split = (p.kblocks + split - 1) / split;
+  p.split = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  p.tiles_m = (int)((g.M + 63) / 64);
+  p.tiles_n = (int)((g.N + (g.paired ? 31 : 63)) / (g.paired ? 32 : 64));
+  p.epi = g.epi;
+  SimtOperand A{g.a.p, g.a.ld, g.a.km ? 1 : 0, e->prec};
+  SimtOperand B{g.b.p, g.b.ld, g.b.km ? 1 : 0, e->prec};
+  dim3 grid(p.tiles_m, p.tiles_n, p.split);
+  gemm_simt_kernel<<<grid, 256, 0, s>>>(A, B, p);
+  return check_launch("gemm_simt_kernel");
+}
+
+// out (fp32, ldo) += alpha * A B^T; split-K with atomics when the output has
+// too few tiles to fill the GPU (the long-K Wgrad / low-rank contractions).
+int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float alpha, cudaStream_t s) {
+  const int tiles = tiles_for(g, e->prec);
+  const int kblocks = (int)((g.K + 63) / 64);
+  if (tiles < 2 * kNumSMs / 3 && kblocks >= 8) {
+    Epilogue ep{};
+    ep.kind = EPI_ATOMIC; ep.out = out; ep.ldo = ldo; ep.alpha = alpha; ep.out_prec = PREC_F32;
+    g.epi = ep;
+    g.split = std::max(1, std::min((kNumSMs + tiles - 1) / tiles, kblocks / 4));
+    if (e->prec == PREC_F32) g.split = std::max(1, std::min(g.split * 4, (int)((g.K + 15) / 16) / 8));
+  } else {
+    g.epi = epi_store(out, ldo, PREC_F32, alpha, 1.f);
+    g.split = 1;
+  }
+  return run_gemm(e, g, s);
+}
+
+int rmsnorm_fwd(mecefo_engine* e, const float* x, const float* g, void* out, float* inv, int64_t rows, int64_t m,
+                cudaStream_t s) {
+  const int warps = 8;
+  rmsnorm_fwd_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(x, g, out, inv, (int)rows, (int)m,
+                                                                                    e->prec);
+  return check_launch("rmsnorm_fwd_kernel");
+}
+
+// dx = resid + rmsnorm_bwd(...); grad_scale (+)= alpha * dscale (if non-null).
+int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const float* inv, const float* d,
+                const float* resid, float* dx, void* dx_lp, float* grad_scale, float alpha, int64_t rows, int64_t m,
+                cudaStream_t s) {
+  const int rpb = 64;
+  const int nblk = (int)((rows + rpb - 1) / rpb);
+  float* partial = nullptr;
+  if (grad_scale) TRY(ws.take((size_t)nblk * m * sizeof(float), reinterpret_cast<void**>(&partial)));
+  const size_t sm = 8 * m * sizeof(float);
+  if (sm > 48 * 1024) {
+    static bool set = false;
+    if (!set) { CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); set = true; }
+  }
+  rmsnorm_bwd_kernel<<<nblk, 256, sm, s>>>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, (int)rows, (int)m, rpb);
+  TRY(check_launch("rmsnorm_bwd_kernel"));
+  if (grad_scale) {
+    colsum_finalize_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(partial, nblk, (int)m, grad_scale, alpha, 1.f);
+    TRY(check_launch("colsum_finalize_kernel"));
+  }
+  return MECEFO_OK;
+}
+
+int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4096);
+  cast_f32_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(src, dst, n, e->prec);
+  return check_launch("cast_f32_kernel");
+}
+
+int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaStream_t s) {
+  const int hd = (int)(e->d.hidden / e->d.heads);
+  const int nseq = (int)(tokens / e->d.seq_len);
+  dim3 grid(nseq * a.H, (a.T + 63) / 64);
+  const size_t per_row = (size_t)(hd + 4) * sizeof(float);
+  size_t sm = backward ? std::max<size_t>(2 * a.T * per_row, 2 * a.T * per_row + 2 * a.T * sizeof(float))
+                       : 2 * (size_t)a.T * per_row;
+  if (sm > 220 * 1024) return set_err(MECEFO_ERR_CONTRACT, "seq_len %d x head_dim %d exceeds the attention smem plan", a.T, hd);
+#define ATTN_CASE(D)                                                                                      \
+  case D: {                                                                                               \
+    if (!backward) {                                                                                      \
+      CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+      attn_fwd_kernel<D><<<grid, 256, sm, s>>>(a);                                                        \
+      return check_launch("attn_fwd_kernel");                                                             \
+    }                                                                                                     \
+    CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    attn_bwd_dq_kernel<D><<<grid, 256, sm, s>>>(a);                                                       \
+    TRY(check_launch("attn_bwd_dq_kernel"));                                                              \
+    attn_bwd_dkv_kernel<D><<<grid, 256, sm, s>>>(a);                                                      \
+    return check_launch("attn_bwd_dkv_kernel");                                                           \
+  }
+  switch (hd) {
+    ATTN_CASE(2)
+    ATTN_CASE(4)
+    ATTN_CASE(8)
+    ATTN_CASE(16)
+    ATTN_CASE(32)
+    ATTN_CASE(64)
+    ATTN_CASE(128)
+    default:
+      return set_err(MECEFO_ERR_CONTRACT, "unsupported head_dim %d (supported: 2..128, powers of two)", hd);
+  }
+#undef ATTN_CASE
+}
+
+AttnDev attn_args(mecefo_engine* e) {
+  AttnDev a{};
+  a.T = (int)e->d.seq_len;
+  a.H = (int)e->d.heads;
+  a.m = (int)e->d.hidden;
+  a.rope = e->d.rope;
+  a.prec = e->prec;
+  a.cosT = e->rope_cos;
+  a.sinT = e->rope_sin;
+  a.scale = (float)(1.0 / std::sqrt((double)(e->d.hidden / e->d.heads)));
+  return a;
+}
+
+int check_tokens(mecefo_engine* e, int64_t tokens) {
+  if (tokens <= 0 || tokens % e->d.seq_len != 0)
+    return set_err(MECEFO_ERR_CONTRACT, "activations of %lld rows do not match seq_len=%lld", (long long)tokens,
+                   (long long)e->d.seq_len);
+  return MECEFO_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* mecefo_last_error(void) { return g_last_error.c_str(); }
+const char* mecefo_version(void) { return "mecefo-b200 0.1 (sm_100a)"; }
+int64_t mecefo_launch_count(void) { return g_launches.load(); }
+
+int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims) {
+  if (!out || !dims) return set_err(MECEFO_ERR_CONTRACT, "null argument");
+  const mecefo_dims& d = *dims;
+  if (d.vocab < 1 || d.hidden < 1 || d.heads < 1 || d.ffn < 1 || d.layers < 1 || d.seq_len < 1)
+    return set_err(MECEFO_ERR_CONTRACT, "dims must be >= 1");
+  if (d.hidden % d.heads != 0) return set_err(MECEFO_ERR_CONTRACT, "hidden must be divisible by heads");
+  if (d.rope && (d.hidden / d.heads) % 2 != 0) return set_err(MECEFO_ERR_CONTRACT, "rotary positions need an even head dim");
+  if (d.precision != MECEFO_PREC_F32 && d.precision != MECEFO_PREC_BF16)
+    return set_err(MECEFO_ERR_CONFIG, "unknown precision %d", d.precision);
+  if (d.precision == MECEFO_PREC_BF16 && (d.hidden % 8 != 0 || d.ffn % 8 != 0 || d.vocab % 8 != 0))
+    return set_err(MECEFO_ERR_CONTRACT,
+                   "bf16 (TMA) mode needs hidden, ffn and vocab to be multiples of 8 (16-byte rows); pad ffn");
+  auto* e = new mecefo_engine();
+  e->d = d;
+  e->prec = d.precision;
+  e->ps = d.precision == MECEFO_PREC_BF16 ? 2 : 4;
+  const int hd = (int)(d.hidden / d.heads);
+  const int half = std::max(1, hd / 2);
+  std::vector<float> c((size_t)d.seq_len * half), sn((size_t)d.seq_len * half);
+  for (int64_t t = 0; t < d.seq_len; ++t)
+    for (int j = 0; j < half; ++j) {
+      const double theta = std::pow(10000.0, -2.0 * j / hd);  // model.py:274
+      const double ang = (double)t * theta;
+      c[t * half + j] = (float)std::cos(ang);
+      sn[t * half + j] = (float)std::sin(ang);
+    }
+  cudaError_t ce = cudaMalloc(&e->rope_cos, c.size() * sizeof(float));
+  if (ce == cudaSuccess) ce = cudaMalloc(&e->rope_sin, sn.size() * sizeof(float));
+  if (ce == cudaSuccess) ce = cudaMemcpy(e->rope_cos, c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMemcpy(e->rope_sin, sn.data(), sn.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    cudaFree(e->rope_cos);
+    cudaFree(e->rope_sin);
+    delete e;
+    return set_err(MECEFO_ERR_CUDA, "engine allocation failed: %s", cudaGetErrorString(ce));
+  }
+  *out = e;
+  return MECEFO_OK;
+}
+
+int mecefo_engine_destroy(mecefo_engine* e) {
+  if (!e) return MECEFO_OK;
+  cudaFree(e->rope_cos);
+  cudaFree(e->rope_sin);
+  delete e;
+  return MECEFO_OK;
+}
+
+size_t mecefo_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t rank_pad) {
+  const int64_t m = e->d.hidden, f = e->d.ffn, H = e->d.heads, ps = e->ps;
+  const int64_t rp = std::max<int32_t>(rank_pad, 16);
+  const int64_t per_tok = (6 * m + 4 * f + 3 * rp) * ps + 16 * m + 8 * H + 64;
+  const int64_t fixed = 3 * std::max(m, f) * rp * (4 + ps) + ((tokens + 63) / 64 + 8) * m * 4 * 2 +
+                        e->d.vocab * 4 + (4 << 20);
+  return (size_t)(tokens * per_tok + fixed);
+}
+
+int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* c, float* y, void* y_c,
+                         int64_t tokens, int32_t mode, void* wsp, size_t ws_bytes, void* stream) {
+  (void)y_c;
+  TRY(check_tokens(e, tokens));
+  if (mode != MECEFO_CACHE_FULL && mode != MECEFO_CACHE_FFN_INPUT_ONLY)
+    return set_err(MECEFO_ERR_CONTRACT, "unknown cache mode %d", mode);
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const bool full = mode == MECEFO_CACHE_FULL;
+  const int64_t b = tokens, m = e->d.hidden, f = e->d.ffn, H = e->d.heads;
+  Ws ws(wsp, ws_bytes);
+  void *h1 = c->h1, *qkv = c->qkv, *ctx = c->ctx, *h2 = c->h2, *act = c->act;
+  float *inv1 = c->inv1, *lse = c->lse, *inv2 = c->inv2;
+  if (!full || !h1) TRY(ws.take(b * m * e->ps, &h1));
+  if (!full || !inv1) TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv1)));
+  if (!full || !qkv) TRY(ws.take(b * 3 * m * e->ps, &qkv));
+  if (!full || !ctx) TRY(ws.take(b * m * e->ps, &ctx));
+  if (!full) lse = nullptr;
+  if (full && !lse) TRY(ws.take(b * H * 4, reinterpret_cast<void**>(&lse)));
+  if (!full || !h2) TRY(ws.take(b * m * e->ps, &h2));
+  if (!full || !inv2) TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv2)));
+  if (!full || !act) TRY(ws.take(b * f * e->ps, &act));
+
+  // h1 = rmsnorm(x) * g_mha; qkv = h1 [Wq;Wk;Wv]^T            (model.py:404, 320-322)
+  TRY(rmsnorm_fwd(e, c->x, lw->norm_mha, h1, inv1, b, m, s));
+  GemmCall g;
+  g.M = b; g.N = 3 * m; g.K = m;
+  g.a = {h1, m, true}; g.b = {lw->w_qkv_c, m, true};
+  g.epi = epi_store(qkv, 3 * m, e->prec);
+  TRY(run_gemm(e, g, s));
+  // causal attention with RoPE -> ctx                         (model.py:323-331)
+  AttnDev a = attn_args(e);
+  a.qkv = qkv; a.ld_qkv = 3 * m; a.ctx = ctx; a.ld_ctx = m; a.lse = lse;
+  TRY(attention(e, false, a, b, s));
+  // x1 = x + ctx Wo^T                                          (model.py:332, 406)
+  g = GemmCall();
+  g.M = b; g.N = m; g.K = m;
+  g.a = {ctx, m, true}; g.b = {lw->w_o_c, m, true};
+  g.epi = epi_store(c->x1, m, PREC_F32, 1.f, 0.f, c->x, m);
+  TRY(run_gemm(e, g, s));
+  // h2 = rmsnorm(x1) * g_ffn; act = silu(h2 Wg^T) * (h2 Wu^T)  (model.py:213-216)
+  TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
+  g = GemmCall();
+  g.M = b; g.N = f; g.K = m;
+  g.a = {h2, m, true}; g.b = {lw->w_gu_c, m, true};
+  g.paired = true; g.pair_off = f;
+  Epilogue ep{};
+  ep.kind = EPI_SWIGLU_FWD; ep.out = act; ep.ldo = f; ep.act_prec = e->prec;
+  if (full && c->gu) { ep.out2 = c->gu; ep.ldo2 = 2 * f; ep.off2 = f; }
+  g.epi = ep;
+  TRY(run_gemm(e, g, s));
+  // y = x1 + act Wd^T                                          (model.py:217, 408)
+  g = GemmCall();
+  g.M = b; g.N = m; g.K = f;
+  g.a = {act, f, true}; g.b = {lw->w_down_c, f, true};
+  g.epi = epi_store(y, m, PREC_F32, 1.f, 0.f, c->x1, m);
+  TRY(run_gemm(e, g, s));
+  return MECEFO_OK;
+}
+
+namespace {
+
+// Low-rank FFN weight gradients (approx.py:24-42, 118-126):
+//   grad[kind] += alpha * d2^T (inp2 V1) V1^T   for kind in (gate, up, down).
+int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, const void* dy_c, const void* h2,
+                       const void* act, const void* dcat, const mecefo_layer_grads* gr, int64_t b, cudaStream_t s) {
+  const int64_t m = e->d.hidden, f = e->d.ffn, rp = pj->rank_pad;
+  const int ps = e->ps;
+  if (rp % 16 != 0) return set_err(MECEFO_ERR_CONTRACT, "rank_pad must be a multiple of 16");
+  // kind -> (d2, ld_d2, out dim, inp2, in dim, grad pointer)
+  struct K { const void* d2; int64_t ldd; int64_t n_out; const void* inp; int64_t n_in; float* grad; };
+  const K kinds[3] = {
+      {dcat, 2 * f, f, h2, m, gr->gu},
+      {dcat ? reinterpret_cast<const uint8_t*>(dcat) + f * ps : nullptr, 2 * f, f, h2, m,
+       gr->gu ? gr->gu + f * m : nullptr},
+      {dy_c, m, m, act, f, gr->down},
+  };
+  void* P;
+  float* Q;
+  void* Qc;
+  TRY(ws.take(b * rp * ps, &P));
+  TRY(ws.take(std::max(m, f) * rp * 4, reinterpret_cast<void**>(&Q)));
+  if (e->prec == PREC_BF16) TRY(ws.take(std::max(m, f) * rp * ps, &Qc));
+  else Qc = Q;
+  for (int k = 0; k < 3; ++k) {
+    const K& kd = kinds[k];
+    if (!kd.grad) continue;
+    if (!pj->v1[k] || !pj->v1t[k]) return set_err(MECEFO_ERR_CONTRACT, "projection basis %d missing", k);
+    // P = inp2 V1  (b, rp)
+    GemmCall g;
+    g.M = b; g.N = rp; g.K = kd.n_in;
+    g.a = {kd.inp, kd.n_in, true}; g.b = {pj->v1t[k], kd.n_in, true};
+    g.epi = epi_store(P, rp, e->prec);
+    TRY(run_gemm(e, g, s));
+    // Q = d2^T P  (n_out, rp), K = b: the long-K "small contraction"
+    CUDA_TRY(cudaMemsetAsync(Q, 0, kd.n_out * rp * 4, s));
+    g = GemmCall();
+    g.M = kd.n_out; g.N = rp; g.K = b;
+    g.a = {kd.d2, kd.ldd, false}; g.b = {P, rp, false};
+    TRY(gemm_accumulate(e, g, Q, rp, 1.f, s));
+    if (e->prec == PREC_BF16) TRY(cast_to_compute(e, Q, Qc, kd.n_out * rp, s));
+    // grad += alpha * Q V1^T  (n_out, n_in), K = rp: the up-projection
+    g = GemmCall();
+    g.M = kd.n_out; g.N = kd.n_in; g.K = rp;
+    g.a = {Qc, rp, true}; g.b = {pj->v1[k], rp, true};
+    g.epi = epi_store(kd.grad, kd.n_in, PREC_F32, gr->alpha_ffn, 1.f);
+    TRY(run_gemm(e, g, s));
+  }
+  return MECEFO_OK;
+}
+
+}  // namespace
+
+int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights* lw, const mecefo_block_cache* c,
+                                   const float* dy, const void* dy_c, float* dx, void* dx_c,
+                                   const mecefo_layer_grads* gr, const mecefo_projection* pj, int64_t tokens, void* wsp,
+                                   size_t ws_bytes, void* stream) {
+  TRY(check_tokens(e, tokens));
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, m = e->d.hidden, f = e->d.ffn;
+  Ws ws(wsp, ws_bytes);
+  mecefo_layer_grads none{};
+  if (!gr) gr = &none;
+  if (!dy_c || e->prec == PREC_F32) {
+    if (e->prec == PREC_F32) dy_c = dy;
+    else {
+      void* t;
+      TRY(ws.take(b * m * e->ps, &t));
+      TRY(cast_to_compute(e, dy, t, b * m, s));
+      dy_c = t;
+    }
+  }
+  void *h2, *d_act, *act, *dcat;
+  float *inv2, *dh;
+  TRY(ws.take(b * m * e->ps, &h2));
+  TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv2)));
+  TRY(ws.take(b * f * e->ps, &d_act));
+  TRY(ws.take(b * f * e->ps, &act));
+  TRY(ws.take(b * 2 * f * e->ps, &dcat));
+  TRY(ws.take(b * m * 4, reinterpret_cast<void**>(&dh)));
+  // recompute h2 = rmsnorm(x1) (approx.py:128 -> model.py:213)
+  TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
+  // d_act = dy Wd  (model.py:248); Wd is (m, f) = B MN-major
+  GemmCall g;
+  g.M = b; g.N = f; g.K = m;
+  g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
+  g.epi = epi_store(d_act, f, e->prec);
+  TRY(run_gemm(e, g, s));
+  // recompute gate/up on the tensor cores; the epilogue forms act and the
+  // SwiGLU backward (model.py:214-216, 250-253): gate/up never touch HBM.
+  g = GemmCall();
+  g.M = b; g.N = f; g.K = m;
+  g.a = {h2, m, true}; g.b = {lw->w_gu_c, m, true};
+  g.paired = true; g.pair_off = f;
+  Epilogue ep{};
+  ep.kind = EPI_SWIGLU_BWD_RECOMP; ep.out = act; ep.ldo = f; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
+  ep.aux = d_act; ep.ldaux = f; ep.act_prec = e->prec;
+  g.epi = ep;
+  TRY(run_gemm(e, g, s));
+  // d_h2 = [d_gate | d_up] [Wg; Wu]  (model.py:258), K = 2f
+  g = GemmCall();
+  g.M = b; g.N = m; g.K = 2 * f;
+  g.a = {dcat, 2 * f, true}; g.b = {lw->w_gu_c, m, false};
+  g.epi = epi_store(dh, m, PREC_F32);
+  TRY(run_gemm(e, g, s));
+  // dx = dy + rmsnorm_bwd(x1, ...)   (model.py:259, approx.py:130)
+  TRY(rmsnorm_bwd(e, ws, c->x1, lw->norm_ffn, inv2, dh, dy, dx, dx_c, gr->norm_ffn, gr->alpha_ffn, b, m, s));
+  // FFN weight gradients
+  if (pj) {
+    TRY(lowrank_ffn_wgrads(e, ws, pj, dy_c, h2, act, dcat, gr, b, s));
+  } else {
+    if (gr->down) {  // g_down = dy^T act (model.py:247)
+      g = GemmCall();
+      g.M = m; g.N = f; g.K = b;
+      g.a = {dy_c, m, false}; g.b = {act, f, false};
+      TRY(gemm_accumulate(e, g, gr->down, f, gr->alpha_ffn, s));
+    }
+    if (gr->gu) {  // [g_gate; g_up] = [d_gate | d_up]^T h2 (model.py:255-256)
+      g = GemmCall();
+      g.M = 2 * f; g.N = m; g.K = b;
+      g.a = {dcat, 2 * f, false}; g.b = {h2, m, false};
+      TRY(gemm_accumulate(e, g, gr->gu, m, gr->alpha_ffn, s));
+    }
+  }
+  return MECEFO_OK;
+}
+
+int mecefo_backward_block_exact(mecefo_engine* e, const mecefo_layer_weights* lw, const mecefo_block_cache* c,
+                                const float* dy, const void* dy_c, float* dx, void* dx_c,
+                                const mecefo_layer_grads* gr, int64_t tokens, void* wsp, size_t ws_bytes,
+                                void* stream) {
+  TRY(check_tokens(e, tokens));
+  if (!c->h1 || !c->qkv || !c->ctx || !c->lse || !c->h2 || !c->inv1 || !c->inv2 || !c->gu || !c->act)
+    return set_err(MECEFO_ERR_CONTRACT, "exact backward requires a full activation cache");
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, m = e->d.hidden, f = e->d.ffn, H = e->d.heads;
+  Ws ws(wsp, ws_bytes);
+  mecefo_layer_grads none{};
+  if (!gr) gr = &none;
+  if (!dy_c || e->prec == PREC_F32) {
+    if (e->prec == PREC_F32) dy_c = dy;
+    else {
+      void* t;
+      TRY(ws.take(b * m * e->ps, &t));
+      TRY(cast_to_compute(e, dy, t, b * m, s));
+      dy_c = t;
+    }
+  }
+  void *dcat, *dx1_c, *dctx, *dqkv;
+  float *dh, *dx1, *dsum;
+  TRY(ws.take(b * 2 * f * e->ps, &dcat));
+  TRY(ws.take(b * m * 4, reinterpret_cast<void**>(&dh)));
+  TRY(ws.take(b * m * 4, reinterpret_cast<void**>(&dx1)));
+  TRY(ws.take(b * m * e->ps, &dx1_c));
+  TRY(ws.take(b * m * e->ps, &dctx));
+  TRY(ws.take(b * 3 * m * e->ps, &dqkv));
+  TRY(ws.take(b * H * 4, reinterpret_cast<void**>(&dsum)));
+  // ---- FFN sub-block (model.py:232-261) ----
+  GemmCall g;
+  g.M = b; g.N = f; g.K = m;
+  g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
+  Epilogue ep{};
+  ep.kind = EPI_SWIGLU_BWD_CACHED; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
+  ep.aux = c->gu; ep.ldaux = 2 * f; ep.offaux = f; ep.act_prec = e->prec;
+  g.epi = ep;
+  TRY(run_gemm(e, g, s));
+  g = GemmCall();
+  g.M = b; g.N = m; g.K = 2 * f;
+  g.a = {dcat, 2 * f, true}; g.b = {lw->w_gu_c, m, false};
+  g.epi = epi_store(dh, m, PREC_F32);
+  TRY(run_gemm(e, g, s));
+  TRY(rmsnorm_bwd(e, ws, c->x1, lw->norm_ffn, c->inv2, dh, dy, dx1, dx1_c, gr->norm_ffn, gr->alpha_ffn, b, m, s));
+  if (gr->down) {
+    g = GemmCall();
+    g.M = m; g.N = f; g.K = b;
+    g.a = {dy_c, m, false}; g.b = {c->act, f, false};
+    TRY(gemm_accumulate(e, g, gr->down, f, gr->alpha_ffn, s));
+  }
+  if (gr->gu) {
+    g = GemmCall();
+    g.M = 2 * f; g.N = m; g.K = b;
+    g.a = {dcat, 2 * f, false}; g.b = {c->h2, m, false};
+    TRY(gemm_accumulate(e, g, gr->gu, m, gr->alpha_ffn, s));
+  }
+  // ---- attention sub-block (model.py:336-368) ----
+  g = GemmCall();  // d_ctx = dx1 Wo
+  g.M = b; g.N = m; g.K = m;
+  g.a = {dx1_c, m, true}; g.b = {lw->w_o_c, m, false};
+  g.epi = epi_store(dctx, m, e->prec);
+  TRY(run_gemm(e, g, s));
+  if (gr->o) {  // g_o = dx1^T ctx
+    g = GemmCall();
+    g.M = m; g.N = m; g.K = b;
+    g.a = {dx1_c, m, false}; g.b = {c->ctx, m, false};
+    TRY(gemm_accumulate(e, g, gr->o, m, gr->alpha_mha, s));
+  }
+  AttnDev a = attn_args(e);
+  a.qkv = c->qkv; a.ld_qkv = 3 * m; a.ctx = c->ctx; a.ld_ctx = m; a.dctx = dctx; a.dqkv = dqkv;
+  a.lse = c->lse; a.dsum = dsum;
+  TRY(attention(e, true, a, b, s));
+  g = GemmCall();  // d_h1 = d_qkv [Wq; Wk; Wv], K = 3m
+  g.M = b; g.N = m; g.K = 3 * m;
+  g.a = {dqkv, 3 * m, true}; g.b = {lw->w_qkv_c, m, false};
+  g.epi = epi_store(dh, m, PREC_F32);
+  TRY(run_gemm(e, g, s));
+  if (gr->qkv) {  // [g_q; g_k; g_v] = d_qkv^T h1
+    g = GemmCall();
+    g.M = 3 * m; g.N = m; g.K = b;
+    g.a = {dqkv, 3 * m, false}; g.b = {c->h1, m, false};
+    TRY(gemm_accumulate(e, g, gr->qkv, m, gr->alpha_mha, s));
+  }
+  // dx = dx1 + rmsnorm_bwd(x, g_mha, inv1, d_h1)   (model.py:433-434)
+  TRY(rmsnorm_bwd(e, ws, c->x, lw->norm_mha, c->inv1, dh, dx1, dx, dx_c, gr->norm_mha, gr->alpha_mha, b, m, s));
+  return MECEFO_OK;
+}
+
+int mecefo_recompute_ffn(mecefo_engine* e, const mecefo_layer_weights* lw, const float* x1, int64_t tokens, void* h2,
+                         float* inv2, void* gate, void* up, void* act, float* down, void* wsp, size_t ws_bytes,
+                         void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, m = e->d.hidden, f = e->d.ffn;
+  Ws ws(wsp, ws_bytes);
+  if (!h2) TRY(ws.take(b * m * e->ps, &h2));
+  if (!inv2) TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv2)));
+  if (!act && down) TRY(ws.take(b * f * e->ps, &act));
+  void* gu = nullptr;
+  if (gate || up) TRY(ws.take(b * 2 * f * e->ps, &gu));
+  TRY(rmsnorm_fwd(e, x1, lw->norm_ffn, h2, inv2, b, m, s));
+  GemmCall g;
+  g.M = b; g.N = f; g.K = m;
+  g.a = {h2, m, true}; g.b = {lw->w_gu_c, m, true};
+  g.paired = true; g.pair_off = f;
+  Epilogue ep{};
+  ep.kind = EPI_SWIGLU_FWD; ep.out = act; ep.ldo = f; ep.out2 = gu; ep.ldo2 = 2 * f; ep.off2 = f; ep.act_prec = e->prec;
+  g.epi = ep;
+  TRY(run_gemm(e, g, s));
+  if (gu) {
+    if (gate) CUDA_TRY(cudaMemcpy2DAsync(gate, f * e->ps, gu, 2 * f * e->ps, f * e->ps, b, cudaMemcpyDeviceToDevice, s));
+    if (up)
+      CUDA_TRY(cudaMemcpy2DAsync(up, f * e->ps, reinterpret_cast<uint8_t*>(gu) + f * e->ps, 2 * f * e->ps, f * e->ps,
+                                 b, cudaMemcpyDeviceToDevice, s));
+  }
+  if (down) {
+    g = GemmCall();
+    g.M = b; g.N = m; g.K = f;
+    g.a = {act, f, true}; g.b = {lw->w_down_c, f, true};
+    g.epi = epi_store(down, m, PREC_F32);
+    TRY(run_gemm(e, g, s));
+  }
+  return MECEFO_OK;
+}
+
+int mecefo_lowrank_wgrad(mecefo_engine* e, const void* g_y, const void* x, const void* v1, float* out, int64_t n_out,
+                         int64_t n_in, int64_t batch, int64_t rank, float alpha, void* wsp, size_t ws_bytes,
+                         void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (n_out < 1 || n_in < 1 || batch < 1 || rank < 1) return set_err(MECEFO_ERR_CONTRACT, "empty lowrank_wgrad operand");
+  Ws ws(wsp, ws_bytes);
+  void* P;
+  float* Q;
+  void* Qc;
+  TRY(ws.take(batch * rank * e->ps, &P));
+  TRY(ws.take(n_out * rank * 4, reinterpret_cast<void**>(&Q)));
+  if (e->prec == PREC_BF16) TRY(ws.take(n_out * rank * e->ps, &Qc));
+  else Qc = Q;
+  // P = x^T V1 (batch, rank): A(i=b, k=in) = x[k, i] (MN-major), B(n=r, k=in) = v1[k, n] (MN-major)
+  GemmCall g;
+  g.M = batch; g.N = rank; g.K = n_in;
+  g.a = {x, batch, false}; g.b = {v1, rank, false};
+  g.epi = epi_store(P, rank, e->prec);
+  TRY(run_gemm(e, g, s));
+  // Q = g_y P (n_out, rank): A = g_y K-major (ld batch), B(n=r, k=b) = P[k, n] MN-major
+  CUDA_TRY(cudaMemsetAsync(Q, 0, n_out * rank * 4, s));
+  g = GemmCall();
+  g.M = n_out; g.N = rank; g.K = batch;
+  g.a = {g_y, batch, true}; g.b = {P, rank, false};
+  TRY(gemm_accumulate(e, g, Q, rank, 1.f, s));
+  if (e->prec == PREC_BF16) TRY(cast_to_compute(e, Q, Qc, n_out * rank, s));
+  // out += alpha Q V1^T: B(n=in, k=r) = v1[n, k] K-major
+  g = GemmCall();
+  g.M = n_out; g.N = n_in; g.K = rank;
+  g.a = {Qc, rank, true}; g.b = {v1, rank, true};
+  g.epi = epi_store(out, n_in, PREC_F32, alpha, 1.f);
+  return run_gemm(e, g, s);
+}
+
+int mecefo_embedding_forward(mecefo_engine* e, const int64_t* tokens, const float* emb, float* x, int64_t n,
+                             void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (n <= 0) return MECEFO_OK;
+  embedding_fwd_kernel<<<(unsigned)n, 128, 0, s>>>(tokens, emb, x, (int)n, (int)e->d.hidden);
+  return check_launch("embedding_fwd_kernel");
+}
+
+int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
+                             const int64_t* targets, int64_t tokens, void* xf, float* inv_f, void* logits, float* loss,
+                             void* wsp, size_t ws_bytes, void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, m = e->d.hidden, V = e->d.vocab;
+  Ws ws(wsp, ws_bytes);
+  float* rows;
+  int* bad;
+  TRY(ws.take(b * 4, reinterpret_cast<void**>(&rows)));
+  TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
+  TRY(rmsnorm_fwd(e, x_last, final_norm, xf, inv_f, b, m, s));
+  GemmCall g;
+  g.M = b; g.N = V; g.K = m;
+  g.a = {xf, m, true}; g.b = {unemb_c, m, true};
+  g.epi = epi_store(logits, V, e->prec);
+  TRY(run_gemm(e, g, s));
+  CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
+  cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
+                                                    bad);
+  TRY(check_launch("cross_entropy_kernel"));
+  mean_kernel<<<1, 1024, 0, s>>>(rows, (int)b, loss);
+  return check_launch("mean_kernel");
+}
+
+int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* final_norm, const float* inv_f,
+                         const void* xf, const void* dlogits, const void* unemb_c, float* dx, void* dx_c,
+                         float* g_final, float* g_unemb, float alpha, int64_t tokens, void* wsp, size_t ws_bytes,
+                         void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, m = e->d.hidden, V = e->d.vocab;
+  Ws ws(wsp, ws_bytes);
+  float* dxf;
+  TRY(ws.take(b * m * 4, reinterpret_cast<void**>(&dxf)));
+  if (g_unemb) {  // g_unemb = dlogits^T xf  (model.py:480)
+    GemmCall g;
+    g.M = V; g.N = m; g.K = b;
+    g.a = {dlogits, V, false}; g.b = {xf, m, false};
+    TRY(gemm_accumulate(e, g, g_unemb, m, alpha, s));
+  }
+  GemmCall g;  // d_xf = dlogits Wun  (model.py:481)
+  g.M = b; g.N = m; g.K = V;
+  g.a = {dlogits, V, true}; g.b = {unemb_c, m, false};
+  g.epi = epi_store(dxf, m, PREC_F32);
+  TRY(run_gemm(e, g, s));
+  return rmsnorm_bwd(e, ws, x_last, final_norm, inv_f, dxf, nullptr, dx, dx_c, g_final, alpha, b, m, s);
+}
+
+int mecefo_embedding_backward(mecefo_engine* e, const int64_t* tokens, const float* dx0, float* g_emb, float alpha,
+                              int64_t n, void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (n <= 0) return MECEFO_OK;
+  embedding_bwd_kernel<<<(unsigned)n, 128, 0, s>>>(tokens, dx0, g_emb, (int)n, (int)e->d.hidden, alpha);
+  return check_launch("embedding_bwd_kernel");
+}
+
+int mecefo_scale_accumulate(const float* src, float* out, int64_t n, float alpha, float beta, void* stream) {
+  if (n <= 0) return MECEFO_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8 * kNumSMs);
+  axpby_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(src, out, n, alpha, beta);
+  return check_launch("axpby_kernel");
+}
+
+int mecefo_cast(mecefo_engine* e, const float* src, void* dst, int64_t n, void* stream) {
+  if (n <= 0) return MECEFO_OK;
+  return cast_to_compute(e, src, dst, n, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream) {
+  if (n <= 0) return MECEFO_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8 * kNumSMs);
+  nonfinite_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(v, n, flag);
+  return check_launch("nonfinite_kernel");
+}
+
+int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t nseg, int64_t max_numel, float* w,
+                      const float* grad, float* m1, float* m2, void* shadow, float beta1, float beta2, float eps,
+                      void* stream) {
+  if (nseg <= 0) return MECEFO_OK;
+  static_assert(sizeof(mecefo_adam_segment) == sizeof(AdamSeg), "segment layout");
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_numel + 255) / 256, 64));
+  dim3 grid((unsigned)bx, (unsigned)nseg);
+  adamw_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const AdamSeg*>(segs), nseg, w, grad, m1, m2, shadow, e ? e->prec : PREC_F32, beta1, beta2,
+      eps);
+  return check_launch("adamw_kernel");
+}
+
+int mecefo_gemm(mecefo_engine* e, int64_t M, int64_t N, int64_t K, const void* a, int64_t lda, int32_t a_kmajor,
+                const void* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha, float beta,
+                void* stream) {
+  GemmCall g;
+  g.M = M; g.N = N; g.K = K;
+  g.a = {a, lda, a_kmajor != 0}; g.b = {b, ldb, b_kmajor != 0};
+  g.epi = epi_store(c, ldc, PREC_F32, alpha, beta);
+  return run_gemm(e, g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,554 @@
+// GEMM engine: C[m, n] = sum_k A(m, k) * B(n, k) with fused epilogues.
+//
+// Two kernels share one epilogue layer:
+//  * gemm_tc_kernel   — bf16 operands on the 5th-gen tensor cores: TMA
+//    (SWIZZLE_128B) -> shared-memory ring -> tcgen05.mma (one elected thread)
+//    -> double-buffered TMEM accumulator -> 4 epilogue warps (tcgen05.ld).
+//    Persistent over output tiles, optional split-K (atomic epilogue).
+//    Operands may be K-major or MN-major, which is what lets every
+//    contraction in the MeCeFO step (Fprop, Dgrad, the long-K Wgrad and the
+//    low-rank d2^T (x V1) V1^T chain) run without transposing activations.
+//  * gemm_simt_kernel — fp32 FFMA path used for the fp32 parity mode
+//    (tcgen05 has no fp32 MMA).
+//
+// "Paired" mode computes two accumulators per output column n: rows n and
+// n + pair_off of B. It is how the gate/up projections share one GEMM while
+// each thread of the epilogue holds matching gate_n and up_n values (SwiGLU
+// epilogues), without an interleaved weight copy.
+#pragma once
+#include "common.cuh"
+#include <cuda.h>
+
+namespace mecefo {
+
+enum EpiKind : int {
+  EPI_STORE = 0,              // out = alpha*acc (+ beta*out) (+ residual); f32 or bf16 out
+  EPI_ATOMIC = 1,             // out += alpha*acc (fp32 atomics; split-K / accumulate)
+  EPI_SWIGLU_FWD = 2,         // paired: act = silu(g)*u -> out; optional gate/up -> out2
+  EPI_SWIGLU_BWD_RECOMP = 3,  // paired (recomputed g,u) + aux = d_act -> act (out), d_gate/d_up (out2)
+  EPI_SWIGLU_BWD_CACHED = 4,  // acc = d_act; aux = cached gate/up -> d_gate/d_up (out2)
+};
+
+struct Epilogue {
+  int kind;
+  void* out;
+  int64_t ldo;
+  int out_prec;
+  float alpha;
+  float beta;
+  const float* residual;
+  int64_t ldr;
+  void* out2;
+  int64_t ldo2;
+  int64_t off2;
+  const void* aux;
+  int64_t ldaux;
+  int64_t offaux;
+  int act_prec;
+};
+
+struct GemmDev {
+  int M, N, K;           // N = logical output columns (pair columns in paired mode)
+  int paired;            // 0/1
+  int64_t pair_off;      // B row offset of the second accumulator (paired)
+  int split;             // number of K splits
+  int kb_per_split;      // k-blocks (of 64) per split
+  int kblocks;           // total k-blocks
+  int tiles_m, tiles_n, num_tiles;
+  Epilogue epi;
+};
+
+// ---------------------------------------------------------------------------
+// Epilogue application on 16 consecutive output columns of one row.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void store16(void* base, int64_t idx, const float* v, int cnt, int prec) {
+  if (prec == PREC_BF16) {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + idx;
+    if (cnt == 16 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      uint4 w[2];
+      uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        wp[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      reinterpret_cast<uint4*>(p)[0] = w[0];
+      reinterpret_cast<uint4*>(p)[1] = w[1];
+    } else {
+      for (int j = 0; j < cnt; ++j) p[j] = f2bf(v[j]);
+    }
+  } else {
+    float* p = reinterpret_cast<float*>(base) + idx;
+    if (cnt == 16 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        reinterpret_cast<float4*>(p)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+      for (int j = 0; j < cnt; ++j) p[j] = v[j];
+    }
+  }
+}
+
+__device__ __forceinline__ void load16(const void* base, int64_t idx, float* v, int cnt, int prec) {
+  if (prec == PREC_BF16) {
+    const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(base) + idx;
+    if (cnt == 16 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      uint4 w[2];
+      w[0] = reinterpret_cast<const uint4*>(p)[0];
+      w[1] = reinterpret_cast<const uint4*>(p)[1];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(w);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float2 f = __bfloat1622float2(h[j]);
+        v[2 * j] = f.x;
+        v[2 * j + 1] = f.y;
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) v[j] = bf2f(p[j]);
+    }
+  } else {
+    const float* p = reinterpret_cast<const float*>(base) + idx;
+    if (cnt == 16 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float4 f = reinterpret_cast<const float4*>(p)[j];
+        v[4 * j] = f.x; v[4 * j + 1] = f.y; v[4 * j + 2] = f.z; v[4 * j + 3] = f.w;
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) v[j] = p[j];
+    }
+  }
+}
+
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// Non-paired epilogue: v holds acc for columns n0..n0+cnt-1 of row r.
+__device__ __forceinline__ void epi_apply(const Epilogue& e, int r, int n0, int cnt, float* v) {
+  if (e.kind == EPI_STORE) {
+    const int64_t idx = (int64_t)r * e.ldo + n0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] *= e.alpha;
+    if (e.beta != 0.f) {
+      float o[16];
+      load16(e.out, idx, o, cnt, PREC_F32);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] += e.beta * o[j];
+    }
+    if (e.residual) {
+      float o[16];
+      load16(e.residual, (int64_t)r * e.ldr + n0, o, cnt, PREC_F32);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] += o[j];
+    }
+    store16(e.out, idx, v, cnt, e.out_prec);
+  } else if (e.kind == EPI_ATOMIC) {
+    float* p = reinterpret_cast<float*>(e.out) + (int64_t)r * e.ldo + n0;
+    for (int j = 0; j < cnt; ++j) red_add_f32(p + j, e.alpha * v[j]);
+  } else if (e.kind == EPI_SWIGLU_BWD_CACHED) {
+    // acc = d_act; aux holds gate (col n) and up (col offaux + n).
+    float g[16], u[16], dg[16], du[16];
+    load16(e.aux, (int64_t)r * e.ldaux + n0, g, cnt, e.act_prec);
+    load16(e.aux, (int64_t)r * e.ldaux + e.offaux + n0, u, cnt, e.act_prec);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float sg = silu_f(g[j]);
+      du[j] = v[j] * sg;                       // d_up = d_act * silu(gate)
+      dg[j] = (v[j] * u[j]) * silu_grad_f(g[j]);  // d_gate = d_act * up * silu'(gate)
+    }
+    store16(e.out2, (int64_t)r * e.ldo2 + n0, dg, cnt, e.act_prec);
+    store16(e.out2, (int64_t)r * e.ldo2 + e.off2 + n0, du, cnt, e.act_prec);
+  }
+}
+
+// Paired epilogue: g = acc of B row n, u = acc of B row n + pair_off.
+__device__ __forceinline__ void epi_apply_pair(const Epilogue& e, int r, int n0, int cnt, float* g, float* u) {
+  float a[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = silu_f(g[j]) * u[j];  // model.py:216
+  if (e.kind == EPI_SWIGLU_FWD) {
+    if (e.out) store16(e.out, (int64_t)r * e.ldo + n0, a, cnt, e.act_prec);
+    if (e.out2) {
+      store16(e.out2, (int64_t)r * e.ldo2 + n0, g, cnt, e.act_prec);
+      store16(e.out2, (int64_t)r * e.ldo2 + e.off2 + n0, u, cnt, e.act_prec);
+    }
+  } else if (e.kind == EPI_SWIGLU_BWD_RECOMP) {
+    float d[16], dg[16], du[16];
+    load16(e.aux, (int64_t)r * e.ldaux + n0, d, cnt, e.act_prec);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      du[j] = d[j] * silu_f(g[j]);                 // model.py:252
+      dg[j] = (d[j] * u[j]) * silu_grad_f(g[j]);   // model.py:251,253
+    }
+    if (e.out) store16(e.out, (int64_t)r * e.ldo + n0, a, cnt, e.act_prec);
+    store16(e.out2, (int64_t)r * e.ldo2 + n0, dg, cnt, e.act_prec);
+    store16(e.out2, (int64_t)r * e.ldo2 + e.off2 + n0, du, cnt, e.act_prec);
+  }
+}
+
+__device__ __forceinline__ void decode_tile(const GemmDev& p, int t, int& mt, int& nt, int& ks) {
+  mt = t % p.tiles_m;
+  int rest = t / p.tiles_m;
+  nt = rest % p.tiles_n;
+  ks = rest / p.tiles_n;
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMA / mbarrier primitives (inline PTX, sm_100a)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 "version 1" format.
+// K-major: 8-row groups 1024 B apart (SBO), rows of 128 B; MN-major: 8-K-row
+// groups 1024 B apart (SBO), 64-element MN chunks `lbo` bytes apart.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;
+constexpr int TC_THREADS = 256;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmDev p) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mt, nt, ks;
+        decode_tile(p, t, mt, nt, ks);
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* a = sA + stage * C::A_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          const int k0 = kb * TC_BK;
+          if (A_KMAJOR) {
+            tma_load_2d(a, &tmA, &full[stage], k0, mt * TC_BM);
+          } else {
+            tma_load_2d(a, &tmA, &full[stage], mt * TC_BM, k0);
+            tma_load_2d(a + 8192, &tmA, &full[stage], mt * TC_BM + 64, k0);
+          }
+          if (B_KMAJOR) {
+            if (!p.paired) {
+              tma_load_2d(b, &tmB, &full[stage], k0, nt * BN);
+            } else {
+              tma_load_2d(b, &tmB, &full[stage], k0, nt * (BN / 2));
+              tma_load_2d(b + (BN / 2) * 128, &tmB, &full[stage], k0, nt * (BN / 2) + (int)p.pair_off);
+            }
+          } else {
+            constexpr int NCH = BN / 64;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+              int col;
+              if (!p.paired)
+                col = nt * BN + c * 64;
+              else
+                col = (c < NCH / 2) ? nt * (BN / 2) + c * 64 : nt * (BN / 2) + (int)p.pair_off + (c - NCH / 2) * 64;
+              tma_load_2d(b + c * 8192, &tmB, &full[stage], col, k0);
+            }
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer (single thread) =====
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
+                                 ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(TC_BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mt, nt, ks;
+        decode_tile(p, t, mt, nt, ks);
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint64_t ad = A_KMAJOR ? make_sdesc(a_addr + k * 32, 16, 1024) : make_sdesc(a_addr + k * 2048, 8192, 1024);
+            const uint64_t bd = B_KMAJOR ? make_sdesc(b_addr + k * 32, 16, 1024) : make_sdesc(b_addr + k * 2048, 8192, 1024);
+            tc_mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== Epilogue warps: TMEM -> registers -> fused epilogue -> global =====
+    const int ew = warp - 4;
+    const int row_in_tile = ew * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mt, nt, ks;
+      decode_tile(p, t, mt, nt, ks);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mt * TC_BM + row_in_tile;
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (!p.paired) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 16; ++c) {
+          float v[16];
+          tmem_ld16(taddr + c * 16, v);
+          const int n0 = nt * BN + c * 16;
+          if (row < p.M && n0 < p.N) epi_apply(p.epi, row, n0, min(16, p.N - n0), v);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float g[16], u[16];
+          tmem_ld16(taddr + c * 16, g);
+          tmem_ld16(taddr + BN / 2 + c * 16, u);
+          const int n0 = nt * (BN / 2) + c * 16;
+          if (row < p.M && n0 < p.N) epi_apply_pair(p.epi, row, n0, min(16, p.N - n0), g, u);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT GEMM (fp32 parity mode; also accepts bf16 operands).
+// 64x64 accumulator tile, BK=16, 256 threads, 4x4 per thread.
+// ---------------------------------------------------------------------------
+
+struct SimtOperand {
+  const void* ptr;
+  int64_t ld;
+  int kmajor;
+  int prec;
+};
+
+__global__ void __launch_bounds__(256) gemm_simt_kernel(SimtOperand A, SimtOperand B, GemmDev p) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  __shared__ float Cs[64][65];
+  const int tid = threadIdx.x;
+  const int ty = tid / 16, tx = tid % 16;
+  const int mt = blockIdx.x, nt = blockIdx.y, ks = blockIdx.z;
+  const int m0 = mt * 64;
+  const int kb0 = ks * p.kb_per_split;  // k-blocks of 16 here
+  const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
+  float acc[4][4] = {};
+  for (int kb = kb0; kb < kb1; ++kb) {
+    const int k0 = kb * 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      int row, kk;
+      if (A.kmajor) { row = e / 16; kk = e % 16; } else { kk = e / 64; row = e % 64; }
+      const int gm = m0 + row, gk = k0 + kk;
+      float va = 0.f;
+      if (gm < p.M && gk < p.K)
+        va = load_as_f32(A.ptr, A.kmajor ? (int64_t)gm * A.ld + gk : (int64_t)gk * A.ld + gm, A.prec);
+      As[kk][row] = va;
+      if (B.kmajor) { row = e / 16; kk = e % 16; } else { kk = e / 64; row = e % 64; }
+      int64_t gn;
+      bool ok;
+      if (!p.paired) {
+        gn = (int64_t)nt * 64 + row;
+        ok = gn < p.N;
+      } else {
+        const int pc = nt * 32 + (row & 31);
+        ok = pc < p.N;
+        gn = pc + ((row >= 32) ? p.pair_off : 0);
+      }
+      const int gk2 = k0 + kk;
+      float vb = 0.f;
+      if (ok && gk2 < p.K)
+        vb = load_as_f32(B.ptr, B.kmajor ? gn * B.ld + gk2 : (int64_t)gk2 * B.ld + gn, B.prec);
+      Bs[kk][row] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Cs[ty * 4 + i][tx * 4 + j] = acc[i][j];
+  __syncthreads();
+  if (!p.paired) {
+    const int row = tid / 4, ch = tid % 4;
+    const int gr = m0 + row, n0 = nt * 64 + ch * 16;
+    if (gr < p.M && n0 < p.N) {
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = Cs[row][ch * 16 + j];
+      epi_apply(p.epi, gr, n0, min(16, p.N - n0), v);
+    }
+  } else if (tid < 128) {
+    const int row = tid / 2, ch = tid % 2;
+    const int gr = m0 + row, n0 = nt * 32 + ch * 16;
+    if (gr < p.M && n0 < p.N) {
+      float g[16], u[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        g[j] = Cs[row][ch * 16 + j];
+        u[j] = Cs[row][32 + ch * 16 + j];
+      }
+      epi_apply_pair(p.epi, gr, n0, min(16, p.N - n0), g, u);
+    }
+  }
+}
+
+}  // namespace mecefo

@@ -1,0 +1,234 @@
+// HBM-bound kernels of the MeCeFO step: RMSNorm forward/backward (fused with
+// the residual add and a deterministic two-stage scale-gradient reduction),
+// embedding gather/scatter, fused softmax-cross-entropy forward+backward,
+// Eq. (1) gradient scale/accumulate, and the multi-tensor AdamW step.
+#pragma once
+#include "common.cuh"
+
+namespace mecefo {
+
+constexpr float kRmsEps = 1e-6f;  // model.py:27
+
+// ---------------------------------------------------------------------------
+// RMSNorm forward: out = (x * inv) * g, inv = 1/sqrt(mean(x^2) + eps).
+// model.py:183-186. One warp per row, float4 loads when aligned.
+// ---------------------------------------------------------------------------
+__global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ g, void* __restrict__ out,
+                                   float* __restrict__ inv_out, int rows, int m, int out_prec) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* xr = x + (int64_t)row * m;
+  float ss = 0.f;
+  const bool vec = ((m & 3) == 0);
+  if (vec) {
+    for (int c = lane * 4; c < m; c += 128) {
+      float4 v = *reinterpret_cast<const float4*>(xr + c);
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+  } else {
+    for (int c = lane; c < m; c += 32) ss += xr[c] * xr[c];
+  }
+  ss = warp_sum(ss);
+  const float inv = 1.f / sqrtf(ss / (float)m + kRmsEps);
+  if (lane == 0 && inv_out) inv_out[row] = inv;
+  if (vec && out_prec == PREC_BF16) {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + (int64_t)row * m;
+    for (int c = lane * 4; c < m; c += 128) {
+      float4 v = *reinterpret_cast<const float4*>(xr + c);
+      float4 s = *reinterpret_cast<const float4*>(g + c);
+      __nv_bfloat162 a = __floats2bfloat162_rn((v.x * inv) * s.x, (v.y * inv) * s.y);
+      __nv_bfloat162 b = __floats2bfloat162_rn((v.z * inv) * s.z, (v.w * inv) * s.w);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&a);
+      w.y = *reinterpret_cast<uint32_t*>(&b);
+      *reinterpret_cast<uint2*>(o + c) = w;
+    }
+  } else {
+    for (int c = lane; c < m; c += 32) store_from_f32(out, (int64_t)row * m + c, (xr[c] * inv) * g[c], out_prec);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RMSNorm backward fused with the residual add (model.py:189-195,
+// approx.py:130): dx = resid + a*inv - x*inv^3*(sum(a*x)/m), a = d*g.
+// Also emits a low-precision copy of dx (the next GEMM operand) and per-block
+// partial column sums of d*x*inv (the scale gradient), reduced by
+// colsum_finalize_kernel in a fixed order (deterministic).
+// Block = 8 warps, each warp one row at a time; block b owns rows
+// [b*rows_per_block, ...).
+// ---------------------------------------------------------------------------
+__global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                   const float* __restrict__ inv, const float* __restrict__ d,
+                                   const float* __restrict__ resid, float* __restrict__ dx, void* __restrict__ dx_lp,
+                                   int lp_prec, float* __restrict__ partial, int rows, int m, int rows_per_block) {
+  extern __shared__ float sh[];  // [8][m] per-warp column partials
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* acc = sh + wid * m;
+  for (int c = lane; c < m; c += 32) acc[c] = 0.f;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(r0 + rows_per_block, rows);
+  for (int row = r0 + wid; row < r1; row += 8) {
+    const float* xr = x + (int64_t)row * m;
+    const float* dr = d + (int64_t)row * m;
+    const float iv = inv[row];
+    float s = 0.f;
+    for (int c = lane; c < m; c += 32) {
+      const float a = dr[c] * g[c];
+      s += a * xr[c];
+      acc[c] += dr[c] * xr[c] * iv;
+    }
+    s = warp_sum(s) / (float)m;
+    const float k = iv * iv * iv * s;
+    for (int c = lane; c < m; c += 32) {
+      float v = dr[c] * g[c] * iv - xr[c] * k;
+      if (resid) v += resid[(int64_t)row * m + c];
+      dx[(int64_t)row * m + c] = v;
+      if (dx_lp) store_from_f32(dx_lp, (int64_t)row * m + c, v, lp_prec);
+    }
+  }
+  __syncthreads();
+  if (partial) {
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += sh[w * m + c];
+      partial[(int64_t)blockIdx.x * m + c] = t;
+    }
+  }
+}
+
+// out[c] = beta*out[c] + alpha * sum_b partial[b, c] (fixed order over b).
+__global__ void colsum_finalize_kernel(const float* __restrict__ partial, int nblocks, int m, float* __restrict__ out,
+                                       float alpha, float beta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  float t = 0.f;
+  for (int b = 0; b < nblocks; ++b) t += partial[(int64_t)b * m + c];
+  out[c] = (beta != 0.f ? beta * out[c] : 0.f) + alpha * t;
+}
+
+// ---------------------------------------------------------------------------
+// Embedding gather / scatter-add (model.py:463, 486-489).
+// ---------------------------------------------------------------------------
+__global__ void embedding_fwd_kernel(const int64_t* __restrict__ tok, const float* __restrict__ emb,
+                                     float* __restrict__ out, int rows, int m) {
+  const int row = blockIdx.x;
+  if (row >= rows) return;
+  const float* e = emb + tok[row] * (int64_t)m;
+  float* o = out + (int64_t)row * m;
+  for (int c = threadIdx.x; c < m; c += blockDim.x) o[c] = e[c];
+}
+
+__global__ void embedding_bwd_kernel(const int64_t* __restrict__ tok, const float* __restrict__ dx,
+                                     float* __restrict__ grad, int rows, int m, float alpha) {
+  const int row = blockIdx.x;
+  if (row >= rows) return;
+  float* gp = grad + tok[row] * (int64_t)m;
+  const float* d = dx + (int64_t)row * m;
+  for (int c = threadIdx.x; c < m; c += blockDim.x) atomicAdd(gp + c, alpha * d[c]);
+}
+
+// ---------------------------------------------------------------------------
+// Fused softmax cross-entropy forward + backward (model.py:492-509).
+// loss_row = logsumexp(z) - z[target]; dlogits = (softmax - onehot) / n,
+// written in place over the logits (same precision). One block per row.
+// ---------------------------------------------------------------------------
+__global__ void cross_entropy_kernel(void* __restrict__ logits, int64_t ld, const int64_t* __restrict__ targets,
+                                     float* __restrict__ loss_rows, int rows, int V, float inv_n, int prec,
+                                     int* __restrict__ bad_target) {
+  __shared__ float red[32];
+  const int row = blockIdx.x;
+  if (row >= rows) return;
+  const int64_t base = (int64_t)row * ld;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, load_as_f32(logits, base + c, prec));
+  mx = block_max(mx, red);
+  float s = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) s += expf(load_as_f32(logits, base + c, prec) - mx);
+  s = block_sum(s, red);
+  const float lse = mx + logf(s);
+  const int64_t t = targets[row];
+  if (t < 0 || t >= V) {
+    if (threadIdx.x == 0) atomicExch(bad_target, 1);
+    return;
+  }
+  const float zt = load_as_f32(logits, base + t, prec);
+  __syncthreads();
+  if (threadIdx.x == 0) loss_rows[row] = lse - zt;
+  const float inv_s = 1.f / s;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float p = expf(load_as_f32(logits, base + c, prec) - mx) * inv_s;
+    store_from_f32(logits, base + c, (p - (c == t ? 1.f : 0.f)) * inv_n, prec);
+  }
+}
+
+// Deterministic mean of per-row losses into out[0] (single block).
+__global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  __shared__ float red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  float t = block_sum((float)s, red);
+  if (threadIdx.x == 0) out[0] = t / (float)n;
+}
+
+// ---------------------------------------------------------------------------
+// Eq. (1): out = beta*out + alpha*src over a flat range (fp32).
+// ---------------------------------------------------------------------------
+__global__ void axpby_kernel(const float* __restrict__ src, float* __restrict__ out, int64_t n, float alpha,
+                             float beta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (beta != 0.f ? beta * out[i] : 0.f) + alpha * src[i];
+}
+
+__global__ void cast_f32_kernel(const float* __restrict__ src, void* __restrict__ dst, int64_t n, int prec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    store_from_f32(dst, i, src[i], prec);
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ v, int64_t n, int* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(v[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-tensor AdamW (optim.py:75-93) with per-parameter step counts and a
+// skip mask (optim.py:96-103). Segments describe each named parameter in the
+// flat buffer; skipped segments are simply not listed by the host.
+// ---------------------------------------------------------------------------
+struct AdamSeg {
+  int64_t offset;
+  int64_t numel;
+  float step_size;   // lr / (1 - beta1^t)
+  float inv_bc2;     // 1 / (1 - beta2^t)
+  float lr_wd;       // lr * weight_decay
+  int pad;
+};
+
+__global__ void adamw_kernel(const AdamSeg* __restrict__ segs, int nseg, float* __restrict__ w,
+                             const float* __restrict__ grad, float* __restrict__ m1, float* __restrict__ m2,
+                             void* __restrict__ shadow, int shadow_prec, float beta1, float beta2, float eps) {
+  // blockIdx.y selects the segment; grid-stride over its elements.
+  const int s = blockIdx.y;
+  if (s >= nseg) return;
+  const AdamSeg sg = segs[s];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < sg.numel; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = sg.offset + j;
+    const float g = grad[i];
+    float mm = m1[i], vv = m2[i];
+    mm = beta1 * mm + (1.f - beta1) * g;
+    vv = beta2 * vv + (1.f - beta2) * (g * g);
+    m1[i] = mm;
+    m2[i] = vv;
+    const float wi = w[i];
+    const float upd = sg.step_size * mm / (sqrtf(vv * sg.inv_bc2) + eps) + sg.lr_wd * wi;
+    const float wn = wi - upd;
+    w[i] = wn;
+    if (shadow) store_from_f32(shadow, i, wn, shadow_prec);
+  }
+}
+
+}  // namespace mecefo
