@@ -179,6 +179,15 @@ int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float*
                              const int64_t* targets, int64_t tokens, void* xf, float* inv_f, void* logits,
                              float* loss, void* ws, size_t ws_bytes, void* stream);
 
+/* model.py:469-471: xf = rmsnorm(x_last) * final_norm; logits = xf unembedding^T. */
+int mecefo_head_logits(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
+                       int64_t tokens, void* xf, float* inv_f, void* logits, void* stream);
+
+/* model.py:492-509 cross_entropy: loss[0] = mean CE; logits are overwritten
+ * in place with dlogits = (softmax - onehot) / tokens. */
+int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens, float* loss,
+                         void* ws, size_t ws_bytes, void* stream);
+
 /* model.py:476-483 head_backward (+ accumulate into g_final_norm/g_unemb). */
 int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* final_norm, const float* inv_f,
                          const void* xf, const void* dlogits, const void* unemb_c, float* dx, void* dx_c,

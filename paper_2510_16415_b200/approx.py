@@ -1,0 +1,151 @@
+"""Cheap backward for nodes running a doubled workload — mirror of faultsim.approx.
+
+(i) the attention backward is skipped (identity path only), (ii) the FFN
+intermediates are recomputed from x1 on the tensor cores with SwiGLU fused
+into the GEMM epilogue, (iii) FFN weight gradients are projected onto the
+top-r right singular subspace, G = d2^T (inp2 V1) V1^T (approx.py:24-42),
+with per-(rank, layer) bases refreshed every `refresh_period` local steps.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib, model as mdl, runtime
+from .errors import ContractViolation
+from .linalg import SvdConfig, top_r_right_singular_vectors
+
+FFN_KINDS = mdl.FFN_WEIGHT_KINDS
+
+
+def _pad16(r: int) -> int:
+    return max(16, (r + 15) // 16 * 16)
+
+
+def lowrank_wgrad(g_y: torch.Tensor, x: torch.Tensor, v1: torch.Tensor, precision: str = "fp32") -> torch.Tensor:
+    """approx.py:24-42: g_y (out, b), x (in, b), v1 (in, r) -> (out, in) fp32,
+    computed as g_y (x^T v1) v1^T in exactly that association order."""
+    for name, t in (("g_y", g_y), ("x", x), ("v1", v1)):
+        if t.ndim != 2:
+            raise ContractViolation(f"{name} must be 2-D, got shape {tuple(t.shape)}")
+    if g_y.shape[1] != x.shape[1]:
+        raise ContractViolation(f"g_y and x batch dims differ: {tuple(g_y.shape)} vs {tuple(x.shape)}")
+    if v1.shape[0] != x.shape[0]:
+        raise ContractViolation(f"v1 rows must match x rows: {tuple(v1.shape)} vs {tuple(x.shape)}")
+    n_out, b = g_y.shape
+    n_in, r = v1.shape
+    cfg = mdl.ModelConfig(vocab=8, hidden=8, heads=1, ffn_intermediate=8, layers=1, seq_len=1)
+    eng = runtime.engine_for(cfg, precision)
+    dt = eng.dtype
+    # Zero-pad the batch and rank dims to 16-byte rows (exact: zeros add nothing).
+    bp, rp = (b + 7) // 8 * 8, (r + 7) // 8 * 8
+    gp = torch.zeros(n_out, bp, dtype=dt, device="cuda")
+    xp = torch.zeros(n_in, bp, dtype=dt, device="cuda")
+    vp = torch.zeros(n_in, rp, dtype=dt, device="cuda")
+    gp[:, :b] = g_y.to("cuda", dt)
+    xp[:, :b] = x.to("cuda", dt)
+    vp[:, :r] = v1.to("cuda", dt)
+    out = torch.zeros(n_out, n_in, dtype=torch.float32, device="cuda")
+    ws, wn = eng.workspace(max(bp, n_out, n_in), _pad16(rp))
+    _lib.call("mecefo_lowrank_wgrad", eng.handle, gp.data_ptr(), xp.data_ptr(), vp.data_ptr(), out.data_ptr(), n_out,
+              n_in, bp, rp, 1.0, ws, wn, runtime.stream_ptr())
+    return out
+
+
+@dataclass
+class ProjectionCache:
+    """approx.py:45-63. `basis[kind]` is V1 (in, r_kind) fp32 on device; the
+    engine operands (compute precision, rank padded to 16) are derived lazily."""
+
+    rank: int
+    refresh_period: int
+    step: int = 0
+    basis: dict = field(default_factory=dict)
+    svd_calls: int = 0
+    refreshes: int = 0
+    _packed: dict = field(default_factory=dict, repr=False)
+
+    def reset(self) -> None:
+        self.step = 0
+        self.basis.clear()
+        self._packed.clear()
+
+    def set_basis(self, kind: str, v1) -> None:
+        """Inject a basis (e.g. the reference's seeded V1 for parity)."""
+        t = torch.as_tensor(v1).to("cuda", torch.float32).contiguous()
+        self.basis[kind] = t
+        self._packed.pop(kind, None)
+
+    def packed(self, precision: str):
+        """Projection struct + keep-alive tensors for the engine."""
+        dt = runtime.compute_dtype(precision)
+        ranks = [int(self.basis[k].shape[1]) for k in FFN_KINDS]
+        rp = _pad16(max(ranks))
+        keep = []
+        v1p, v1tp = [], []
+        for k in FFN_KINDS:
+            key = (k, precision, rp)
+            if key not in self._packed:
+                b = self.basis[k]
+                n_in, r = b.shape
+                v = torch.zeros(n_in, rp, dtype=dt, device=b.device)
+                v[:, :r] = b.to(dt)
+                self._packed[key] = (v, v.t().contiguous())
+            v, vt = self._packed[key]
+            keep += [v, vt]
+            v1p.append(v.data_ptr())
+            v1tp.append(vt.data_ptr())
+        st = _lib.Projection((ctypes.c_int32 * 3)(*ranks), rp, (ctypes.c_void_p * 3)(*v1p),
+                             (ctypes.c_void_p * 3)(*v1tp))
+        return st, keep, rp
+
+
+def refresh_projections(cache: ProjectionCache, lw: mdl.LayerWeights, svd: SvdConfig, budgeted: bool = False) -> None:
+    """approx.py:66-87: refresh iff step % period == 0 or no basis; does not
+    advance the step counter."""
+    if cache.refresh_period < 1:
+        raise ContractViolation("refresh_period must be >= 1")
+    if cache.step % cache.refresh_period != 0 and cache.basis:
+        return
+    cache.refreshes += 1
+    for kind in FFN_KINDS:
+        w = lw.kind(kind)
+        rank = min(cache.rank, w.shape[1])
+        cfg = SvdConfig(rank=rank, tolerance=svd.tolerance, max_iterations=svd.max_iterations, seed=svd.seed)
+        cache.set_basis(kind, top_r_right_singular_vectors(w, cfg, budgeted=budgeted))
+        cache.svd_calls += 1
+
+
+def recompute_ffn(lw: mdl.LayerWeights, x1) -> dict:
+    """approx.py:90-96: same kernel as the forward, so bit-identical."""
+    return mdl.ffn_forward(lw, x1)
+
+
+def backward_block_neighbor(cfg: mdl.ModelConfig, lw: mdl.LayerWeights, cache: mdl.BlockCache, dy,
+                            proj: ProjectionCache | None = None, svd: SvdConfig | None = None):
+    """approx.py:99-134. Returns (dx, {gate, up, down, norm_ffn}); advances
+    proj.step by one."""
+    if cache.mode != mdl.CACHE_FFN_INPUT_ONLY:
+        raise ContractViolation("neighbor backward requires an ffn-input-only cache")
+    dy2 = mdl._to_2d(cfg, dy)
+    eng = runtime.engine_for(cfg, lw.precision)
+    b = dy2.shape[0]
+    pst, keep, rp = None, None, 16
+    if proj is not None:
+        if svd is None:
+            raise ContractViolation("projection refresh needs an SvdConfig")
+        refresh_projections(proj, lw, svd)
+        pst, keep, rp = proj.packed(lw.precision)
+    dx = torch.empty_like(dy2)
+    g = mdl._grad_buffers(cfg, dy2.device, mha=False)
+    ws, wn = eng.workspace(b, rp)
+    _lib.call("mecefo_backward_block_neighbor", eng.handle, ctypes.byref(lw.struct()), ctypes.byref(cache.struct()),
+              dy2.data_ptr(), None, dx.data_ptr(), None, ctypes.byref(mdl._grads_struct(g)),
+              ctypes.byref(pst) if pst is not None else None, b, ws, wn, runtime.stream_ptr())
+    del keep
+    if proj is not None:
+        proj.step += 1
+    return dx.reshape(dy.shape), mdl._unpack_grads(cfg, g)

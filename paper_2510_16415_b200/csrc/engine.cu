@@ -784,28 +784,40 @@ int mecefo_embedding_forward(mecefo_engine* e, const int64_t* tokens, const floa
   return check_launch("embedding_fwd_kernel");
 }
 
-int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
-                             const int64_t* targets, int64_t tokens, void* xf, float* inv_f, void* logits, float* loss,
-                             void* wsp, size_t ws_bytes, void* stream) {
+int mecefo_head_logits(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
+                       int64_t tokens, void* xf, float* inv_f, void* logits, void* stream) {
   auto s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t b = tokens, m = e->d.hidden, V = e->d.vocab;
-  Ws ws(wsp, ws_bytes);
-  float* rows;
-  int* bad;
-  TRY(ws.take(b * 4, reinterpret_cast<void**>(&rows)));
-  TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
   TRY(rmsnorm_fwd(e, x_last, final_norm, xf, inv_f, b, m, s));
   GemmCall g;
   g.M = b; g.N = V; g.K = m;
   g.a = {xf, m, true}; g.b = {unemb_c, m, true};
   g.epi = epi_store(logits, V, e->prec);
-  TRY(run_gemm(e, g, s));
+  return run_gemm(e, g, s);
+}
+
+int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens, float* loss,
+                         void* wsp, size_t ws_bytes, void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, V = e->d.vocab;
+  Ws ws(wsp, ws_bytes);
+  float* rows;
+  int* bad;
+  TRY(ws.take(b * 4, reinterpret_cast<void**>(&rows)));
+  TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
   cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
                                                     bad);
   TRY(check_launch("cross_entropy_kernel"));
   mean_kernel<<<1, 1024, 0, s>>>(rows, (int)b, loss);
   return check_launch("mean_kernel");
+}
+
+int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
+                             const int64_t* targets, int64_t tokens, void* xf, float* inv_f, void* logits, float* loss,
+                             void* wsp, size_t ws_bytes, void* stream) {
+  TRY(mecefo_head_logits(e, x_last, final_norm, unemb_c, tokens, xf, inv_f, logits, stream));
+  return mecefo_cross_entropy(e, logits, targets, tokens, loss, wsp, ws_bytes, stream);
 }
 
 int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* final_norm, const float* inv_f,
