@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""MeCeFO degraded-step throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): LLaMA-60M (vocab 32000, hidden 512,
+8 heads, FFN 1376, 8 layers), seq 256, 32 sequences (8192 tokens) per
+microbatch, low-rank FFN Wgrads r=128, bf16 operands / fp32 accumulation.
+
+A "step" is one MeCeFO training iteration of the whole job: R logical DP
+ranks (R = max(2, N) with N GPUs), rank 1 failed, so its ring neighbour runs
+BOTH microbatches with the approximate backward (skip-MHA, FFN recompute,
+low-rank Wgrad), every other GPU runs its own microbatch exactly; Eq. (1)
+all-reduce over NVLink (N > 1) and the fused AdamW step with the Eq. (1)
+skip list. At N = 1 the GPU is the neighbour of an (emulated) failed rank.
+
+value  = R * 8192 tokens per step / step time (device-timed, max over ranks,
+         inputs resident in HBM).
+e2e    = same through the public API with tokens copied from pinned host
+         memory every step and the loss read back every step.
+Also reported: the fault-free step (every GPU one exact microbatch) and the
+instantaneous MeCeFO drop, the dominant kernel's roofline (CUDA events in the
+timed region), the CPU reference step (oracle port) on this host, clocks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s (8×B200) fault-free vs under failures; MeCeFO throughput drop %"
+WORKLOAD = "LLaMA-60M synthetic seq 256, neighbour runs 2 microbatches with low-rank FFN grads r=128 (configs[1])"
+C1 = dict(vocab=32000, hidden=512, heads=8, ffn=1376, layers=8, seq_len=256)
+SEQS = 32
+RANK = 128
+FAILED = (1,)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm: the oracle port of the reference step on host cores
+# --------------------------------------------------------------------------
+
+def cpu_reference_sample(seqs: int = 2, passes: int = 4, min_seconds: float = 8.0):
+    """Time the float64 numpy port of the reference rank pass (all layers lean,
+    injected orthonormal bases, SVD excluded) at the C1 shapes."""
+    from oracle import model_ref as R
+
+    d = R.Dims(vocab=C1["vocab"], hidden=C1["hidden"], heads=C1["heads"], ffn=C1["ffn"], layers=C1["layers"],
+               seq_len=C1["seq_len"])
+    W = R.init_params(d, 0)
+    rng = np.random.Generator(np.random.PCG64(7))
+    bases = {}
+    for l in range(d.layers):
+        bases[l] = {}
+        for k, n_in in (("gate", d.hidden), ("up", d.hidden), ("down", d.ffn)):
+            q, _ = np.linalg.qr(rng.normal(size=(n_in, min(RANK, n_in))))
+            bases[l][k] = q
+    tokens = rng.integers(0, d.vocab, size=(seqs, d.seq_len))
+    targets = rng.integers(0, d.vocab, size=(seqs, d.seq_len))
+    modes = ["ffn_input_only"] * d.layers
+    t0 = time.perf_counter()
+    n = 0
+    while n < passes or time.perf_counter() - t0 < min_seconds:
+        R.rank_pass(d, W, tokens, targets, modes, bases)
+        n += 1
+        if time.perf_counter() - t0 > 60:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n * seqs * d.seq_len / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{n} lean rank passes x {seqs} seq x {d.seq_len} tok at C1 shapes (fp64 numpy oracle, "
+                      f"injected V1, SVD excluded), {dt:.1f}s"}
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    from oracle import model_ref  # noqa: F401  (oracle is test/baseline infrastructure)
+
+    passes_per_step = 1
+    vals = []
+    for _ in range(max(0, args.warmup)):
+        cpu_reference_sample(seqs=2, passes=passes_per_step, min_seconds=0.0)
+    t0 = time.perf_counter()
+    toks = 0
+    for _ in range(args.steps):
+        r = cpu_reference_sample(seqs=2, passes=passes_per_step, min_seconds=0.0)
+        vals.append(r["value"])
+        toks += 2 * C1["seq_len"] * passes_per_step
+    dt = time.perf_counter() - t0
+    v = toks / dt
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / max(1, args.steps),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (uniform tokens, PCG64)",
+           "config": {"workload": WORKLOAD, "sample": "one lean rank pass of 2 sequences per step"},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                            "sample": "fp64 numpy oracle port of faultsim._rank_pass, all layers lean, 2 seq/step"},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+
+class ClockSampler:
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    o = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    parts = [p.strip() for p in o.stdout.strip().split(",")]
+                    if len(parts) >= 6:
+                        self.samples.append(parts)
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fault-free", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no extras)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+
+    from paper_2510_16415_b200 import _lib, engine as E, model as mdl
+    from paper_2510_16415_b200.linalg import SvdConfig
+
+    cfg = mdl.ModelConfig(vocab=C1["vocab"], hidden=C1["hidden"], heads=C1["heads"], ffn_intermediate=C1["ffn"],
+                          layers=C1["layers"], seq_len=C1["seq_len"])
+    R = max(2, world)
+    b = SEQS * cfg.seq_len
+    eng = E.StepEngine(cfg, precision=args.precision, seqs_per_microbatch=SEQS, r=RANK, tau=100, seed=0,
+                       svd=SvdConfig(rank=RANK, tolerance=1e-3, max_iterations=8, seed=23), svd_budgeted=True,
+                       group=group)
+    lib = _lib.load()
+
+    # synthetic LLaMA-shaped batches per logical rank (uniform tokens, PCG64)
+    host_batches, dev_batches = {}, {}
+    for j in range(R):
+        g = np.random.Generator(np.random.PCG64(1000 + j))
+        tk = torch.from_numpy(g.integers(0, cfg.vocab, size=(SEQS, cfg.seq_len))).pin_memory()
+        tg = torch.from_numpy(g.integers(0, cfg.vocab, size=(SEQS, cfg.seq_len))).pin_memory()
+        host_batches[j] = (tk, tg)
+        dev_batches[j] = (tk.cuda(), tg.cuda())
+
+    def plan(failed, batches):
+        route, lean, alpha_mha, skip = E.ring_plan(R, set(failed), cfg.layers)
+        me = rank  # GPU index
+        mbs = []
+        for j in range(R):
+            if route[j] != me:
+                continue
+            if world == 1 and j >= 1 and not failed:
+                continue  # fault-free at N=1: logical rank 1 lives on the absent GPU 1
+            tk, tg = batches[j]
+            mbs.append(E.Microbatch(rank=j, tokens=tk, targets=tg, lean=[lean[j]] * cfg.layers,
+                                    alpha_mha=[None if lean[j] else alpha_mha] * cfg.layers, alpha_ffn=1.0 / R,
+                                    alpha_global=1.0 / R))
+        return mbs, skip
+
+    degraded, skip_d = plan(FAILED, dev_batches)
+    fault_free, skip_f = plan((), dev_batches)
+    degraded_e2e, _ = plan(FAILED, host_batches)
+    lr = 1e-4
+
+    def barrier():
+        if group is not None:
+            dist.barrier()
+
+    def timed(mbs, skip, steps, e2e=False, profile=False):
+        barrier()
+        torch.cuda.synchronize()
+        if profile:
+            lib.mecefo_profile_enable(1)
+        n0 = lib.mecefo_launch_count()
+        t_wall = time.perf_counter()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(steps):
+            losses = eng.step(mbs, R, lr, skip=skip, check=False)
+            if e2e:
+                losses.cpu()  # D2H read of the step's result
+        en.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t_wall
+        launches = lib.mecefo_launch_count() - n0
+        ms = st.elapsed_time(en)
+        barrier()
+        if group is not None:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches, wall
+
+    # warm-up (includes the first projection refresh of every lean layer)
+    for _ in range(args.warmup):
+        eng.step(degraded, R, lr, skip=skip_d, check=False)
+    torch.cuda.synchronize()
+    if args.profile_only:
+        ms, _, _ = timed(degraded, skip_d, args.steps)
+        if rank == 0:
+            print(json.dumps({"profile_only": True, "ms_per_step": ms / args.steps}), flush=True)
+        return
+
+    with ClockSampler(local) as clk:
+        ms, launches, wall = timed(degraded, skip_d, args.steps, profile=True)
+    tokens_per_step = R * b
+    value = tokens_per_step * args.steps / (ms / 1000.0)
+
+    # dominant kernel roofline from the live profile of the timed region
+    n = lib.mecefo_profile_count()
+    import ctypes
+
+    agg = {}
+    for i in range(n):
+        tag = ctypes.c_char_p()
+        kms = ctypes.c_float()
+        fl = ctypes.c_double()
+        by = ctypes.c_double()
+        _lib.check(lib.mecefo_profile_record(i, ctypes.byref(tag), ctypes.byref(kms), ctypes.byref(fl),
+                                             ctypes.byref(by)))
+        a = agg.setdefault(tag.value.decode(), [0.0, 0, 0.0, 0.0])
+        a[0] += kms.value
+        a[1] += 1
+        a[2] += fl.value
+        a[3] += by.value
+    lib.mecefo_profile_enable(0)
+    hbm, bf16, bf16_sus, peak_src = _peaks()
+    top = sorted(agg.items(), key=lambda kv: -kv[1][0])
+    roofline = None
+    kernels = []
+    for tag, (tms, cnt, fl, by) in top[:12]:
+        kernels.append({"tag": tag, "ms_total": round(tms, 3), "launches": cnt, "share": round(tms / ms, 4),
+                        "tflops": round(fl / (tms / 1e3) / 1e12, 1) if fl else None,
+                        "gbs": round(by / (tms / 1e3) / 1e9, 1)})
+    if top:
+        tag, (tms, cnt, fl, by) = top[0]
+        avg_s = tms / cnt / 1e3
+        if fl > 0:
+            ach = fl / cnt / avg_s / 1e12
+            roofline = {"kernel": tag, "bound": "tensor", "achieved": round(ach, 1), "peak": bf16_sus,
+                        "unit": "TFLOP/s", "frac": round(ach / bf16_sus, 4), "traffic": None,
+                        "per_launch": f"{fl / cnt / 1e9:.3f} GFLOP algorithmic (2*M*N*K)",
+                        "peak_source": f"{peak_src} bf16 sustained", "share_of_step": round(tms / ms, 4)}
+        else:
+            ach = by / cnt / avg_s / 1e9
+            roofline = {"kernel": tag, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 4), "traffic": None,
+                        "per_launch": f"{by / cnt / 1e6:.2f} MB algorithmic", "peak_source": peak_src,
+                        "share_of_step": round(tms / ms, 4)}
+
+    # fault-free step (every GPU one exact microbatch) and instantaneous drop
+    ff_value = None
+    if not args.no_fault_free:
+        for _ in range(2):
+            eng.step(fault_free, R, lr, skip=skip_f, check=False)
+        ms_ff, _, _ = timed(fault_free, skip_f, args.steps)
+        ff_value = tokens_per_step * args.steps / (ms_ff / 1000.0)
+
+    # end-to-end through the public API: H2D of inputs + D2H of the loss per step
+    for _ in range(1):
+        eng.step(degraded_e2e, R, lr, skip=skip_d, check=False)
+    ms_e2e, _, _ = timed(degraded_e2e, skip_d, args.steps, e2e=True)
+    e2e_value = tokens_per_step * args.steps / (ms_e2e / 1000.0)
+    h2d = sum(2 * mb.tokens.numel() * 8 for mb in degraded_e2e)
+    loss_ok = bool(torch.isfinite(eng.losses).all().item())
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample()
+        except Exception as exc:  # pragma: no cover
+            cpu = {"error": str(exc)}
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision, "impl": "ours",
+        "data": "synthetic (uniform tokens in [0,32000), PCG64 seeds 1000+j; weights = reference init_weights seed 0)",
+        "config": {"workload": WORKLOAD, "model": "LLaMA-60M", "global_batch": R * SEQS, "seq_len": cfg.seq_len,
+                   "microbatch_tokens": b, "logical_ranks": R, "failed_ranks": list(FAILED), "rank_r": RANK,
+                   "parallelism": f"dp{world} (MeCeFO ring, NDB neighbour)", "l2": "inputs larger than L2 "
+                   "(per-step activations + logits > 126 MB)", "refresh_period": 100},
+        "fault_free_tokens_per_s": round(ff_value, 1) if ff_value else None,
+        "drop_pct_instantaneous": round(100.0 * (1.0 - value / ff_value), 2) if ff_value else None,
+        "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4 * R},
+        "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
+        "clocks": clk.summary(), "loss_finite": loss_ok, "wall_s_timed": round(wall, 3),
+    }
+    print(json.dumps(out), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

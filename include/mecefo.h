@@ -224,6 +224,13 @@ int mecefo_gemm(mecefo_engine* e, int64_t M, int64_t N, int64_t K, const void* a
 /* Number of kernels this library has launched (evidence counter). */
 int64_t mecefo_launch_count(void);
 
+/* Launch profiler (CUDA events around every kernel group, tagged with its
+ * algorithmic FLOPs and HBM bytes). enable(1) clears and starts recording,
+ * enable(0) stops; record(i) synchronizes on record i's end event. */
+int mecefo_profile_enable(int32_t on);
+int64_t mecefo_profile_count(void);
+int mecefo_profile_record(int64_t i, const char** tag, float* ms, double* flops, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -161,6 +161,11 @@ _SIGNATURES = {
         [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_float,
          c_float, c_void_p],
     ),
+    "mecefo_profile_enable": (c_int, [c_int32]),
+    "mecefo_profile_count": (c_int64, []),
+    "mecefo_profile_record": (
+        c_int, [c_int64, POINTER(c_char_p), POINTER(c_float), POINTER(ctypes.c_double), POINTER(ctypes.c_double)],
+    ),
     "mecefo_gemm": (
         c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int32, c_void_p,

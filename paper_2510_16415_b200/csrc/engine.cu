@@ -58,6 +58,48 @@ int check_launch(const char* what) {
   return MECEFO_OK;
 }
 
+// Optional launch profiler: CUDA events around each kernel (or fused
+// kernel group) tagged with its algorithmic FLOPs and HBM bytes. Enabled by
+// bench.py over its timed region; off by default (zero overhead).
+struct ProfRec {
+  const char* tag;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t ev() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+};
+Profiler g_prof;
+std::mutex g_prof_mu;
+
+struct ProfScope {
+  int64_t idx = -1;
+  cudaStream_t s;
+  ProfScope(const char* tag, double flops, double bytes, cudaStream_t st) : s(st) {
+    if (!g_prof.on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.recs.push_back(ProfRec{tag, g_prof.ev(), g_prof.ev(), flops, bytes});
+    idx = (int64_t)g_prof.recs.size() - 1;
+    cudaEventRecord(g_prof.recs[idx].a, s);
+  }
+  ~ProfScope() {
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (idx < (int64_t)g_prof.recs.size()) cudaEventRecord(g_prof.recs[idx].b, s);
+  }
+};
+
 // Bump allocator over the caller's workspace.
 struct Ws {
   uint8_t* base;
@@ -162,6 +204,7 @@ struct GemmCall {
   int64_t pair_off = 0;
   Epilogue epi{};
   int split = 1;
+  const char* tag = "gemm";
 };
 
 Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, float beta = 0.f,
@@ -226,6 +269,11 @@ int tiles_for(const GemmCall& g, int prec) {
 
 int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return MECEFO_OK;
+  const double ncols = (double)(g.paired ? 2 * g.N : g.N);
+  const double out_bytes = g.epi.kind == EPI_STORE ? (g.epi.out_prec == PREC_BF16 ? 2.0 : 4.0) * (1 + (g.epi.beta != 0.f) + (g.epi.residual != nullptr))
+                         : (g.epi.kind == EPI_ATOMIC ? 8.0 : 3.0 * e->ps);
+  ProfScope prof(g.tag, 2.0 * g.M * ncols * g.K,
+                 (double)e->ps * ((double)g.M * g.K + ncols * g.K) + out_bytes * (double)g.M * (double)g.N, s);
   if (g.split > 1 && g.epi.kind != EPI_ATOMIC)
     return set_err(MECEFO_ERR_CONSISTENCY, "split-K requires the atomic epilogue");
   if (e->prec == PREC_BF16) {
@@ -273,6 +321,7 @@ int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float
 
 int rmsnorm_fwd(mecefo_engine* e, const float* x, const float* g, void* out, float* inv, int64_t rows, int64_t m,
                 cudaStream_t s) {
+  ProfScope prof("rmsnorm_fwd", 0.0, (double)rows * m * (4 + e->ps) + 4.0 * rows, s);
   const int warps = 8;
   rmsnorm_fwd_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(x, g, out, inv, (int)rows, (int)m,
                                                                                     e->prec);
@@ -283,6 +332,7 @@ int rmsnorm_fwd(mecefo_engine* e, const float* x, const float* g, void* out, flo
 int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const float* inv, const float* d,
                 const float* resid, float* dx, void* dx_lp, float* grad_scale, float alpha, int64_t rows, int64_t m,
                 cudaStream_t s) {
+  ProfScope prof("rmsnorm_bwd", 0.0, (double)rows * m * (12 + (resid ? 4 : 0) + 4 + (dx_lp ? e->ps : 0)), s);
   const int rpb = 64;
   const int nblk = (int)((rows + rpb - 1) / rpb);
   float* partial = nullptr;
@@ -308,6 +358,8 @@ int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cu
 }
 
 int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaStream_t s) {
+  ProfScope prof(backward ? "attn_bwd" : "attn_fwd", (backward ? 4.0 : 2.0) * tokens * a.T * a.m,
+                 (double)tokens * a.m * e->ps * (backward ? 9 : 4), s);
   const int hd = (int)(e->d.hidden / e->d.heads);
   const int nseq = (int)(tokens / e->d.seq_len);
   dim3 grid(nseq * a.H, (a.T + 63) / 64);
@@ -373,6 +425,31 @@ extern "C" {
 const char* mecefo_last_error(void) { return g_last_error.c_str(); }
 const char* mecefo_version(void) { return "mecefo-b200 0.1 (sm_100a)"; }
 int64_t mecefo_launch_count(void) { return g_launches.load(); }
+
+int mecefo_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.on = on != 0;
+  g_prof.recs.clear();
+  g_prof.next = 0;
+  return MECEFO_OK;
+}
+
+int64_t mecefo_profile_count(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  return (int64_t)g_prof.recs.size();
+}
+
+int mecefo_profile_record(int64_t i, const char** tag, float* ms, double* flops, double* bytes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (i < 0 || i >= (int64_t)g_prof.recs.size()) return set_err(MECEFO_ERR_CONTRACT, "profile index out of range");
+  const ProfRec& r = g_prof.recs[i];
+  CUDA_TRY(cudaEventSynchronize(r.b));
+  CUDA_TRY(cudaEventElapsedTime(ms, r.a, r.b));
+  *tag = r.tag;
+  *flops = r.flops;
+  *bytes = r.bytes;
+  return MECEFO_OK;
+}
 
 int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims) {
   if (!out || !dims) return set_err(MECEFO_ERR_CONTRACT, "null argument");
@@ -459,6 +536,7 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   g.M = b; g.N = 3 * m; g.K = m;
   g.a = {h1, m, true}; g.b = {lw->w_qkv_c, m, true};
   g.epi = epi_store(qkv, 3 * m, e->prec);
+  g.tag = "fwd.qkv";
   TRY(run_gemm(e, g, s));
   // causal attention with RoPE -> ctx                         (model.py:323-331)
   AttnDev a = attn_args(e);
@@ -469,6 +547,7 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   g.M = b; g.N = m; g.K = m;
   g.a = {ctx, m, true}; g.b = {lw->w_o_c, m, true};
   g.epi = epi_store(c->x1, m, PREC_F32, 1.f, 0.f, c->x, m);
+  g.tag = "fwd.o_residual";
   TRY(run_gemm(e, g, s));
   // h2 = rmsnorm(x1) * g_ffn; act = silu(h2 Wg^T) * (h2 Wu^T)  (model.py:213-216)
   TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
@@ -480,12 +559,14 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   ep.kind = EPI_SWIGLU_FWD; ep.out = act; ep.ldo = f; ep.act_prec = e->prec;
   if (full && c->gu) { ep.out2 = c->gu; ep.ldo2 = 2 * f; ep.off2 = f; }
   g.epi = ep;
+  g.tag = "fwd.gu_swiglu";
   TRY(run_gemm(e, g, s));
   // y = x1 + act Wd^T                                          (model.py:217, 408)
   g = GemmCall();
   g.M = b; g.N = m; g.K = f;
   g.a = {act, f, true}; g.b = {lw->w_down_c, f, true};
   g.epi = epi_store(y, m, PREC_F32, 1.f, 0.f, c->x1, m);
+  g.tag = "fwd.down_residual";
   TRY(run_gemm(e, g, s));
   return MECEFO_OK;
 }
@@ -523,12 +604,14 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
     g.M = b; g.N = rp; g.K = kd.n_in;
     g.a = {kd.inp, kd.n_in, true}; g.b = {pj->v1t[k], kd.n_in, true};
     g.epi = epi_store(P, rp, e->prec);
+    g.tag = "lowrank.P";
     TRY(run_gemm(e, g, s));
     // Q = d2^T P  (n_out, rp), K = b: the long-K "small contraction"
     CUDA_TRY(cudaMemsetAsync(Q, 0, kd.n_out * rp * 4, s));
     g = GemmCall();
     g.M = kd.n_out; g.N = rp; g.K = b;
     g.a = {kd.d2, kd.ldd, false}; g.b = {P, rp, false};
+    g.tag = "lowrank.Q";
     TRY(gemm_accumulate(e, g, Q, rp, 1.f, s));
     if (e->prec == PREC_BF16) TRY(cast_to_compute(e, Q, Qc, kd.n_out * rp, s));
     // grad += alpha * Q V1^T  (n_out, n_in), K = rp: the up-projection
@@ -536,6 +619,7 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
     g.M = kd.n_out; g.N = kd.n_in; g.K = rp;
     g.a = {Qc, rp, true}; g.b = {pj->v1[k], rp, true};
     g.epi = epi_store(kd.grad, kd.n_in, PREC_F32, gr->alpha_ffn, 1.f);
+    g.tag = "lowrank.up_proj";
     TRY(run_gemm(e, g, s));
   }
   return MECEFO_OK;
@@ -577,6 +661,7 @@ int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights*
   g.M = b; g.N = f; g.K = m;
   g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
   g.epi = epi_store(d_act, f, e->prec);
+  g.tag = "nbr.d_act";
   TRY(run_gemm(e, g, s));
   // recompute gate/up on the tensor cores; the epilogue forms act and the
   // SwiGLU backward (model.py:214-216, 250-253): gate/up never touch HBM.
@@ -588,12 +673,14 @@ int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights*
   ep.kind = EPI_SWIGLU_BWD_RECOMP; ep.out = act; ep.ldo = f; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
   ep.aux = d_act; ep.ldaux = f; ep.act_prec = e->prec;
   g.epi = ep;
+  g.tag = "nbr.gu_recompute_swiglu_bwd";
   TRY(run_gemm(e, g, s));
   // d_h2 = [d_gate | d_up] [Wg; Wu]  (model.py:258), K = 2f
   g = GemmCall();
   g.M = b; g.N = m; g.K = 2 * f;
   g.a = {dcat, 2 * f, true}; g.b = {lw->w_gu_c, m, false};
   g.epi = epi_store(dh, m, PREC_F32);
+  g.tag = "nbr.d_h2";
   TRY(run_gemm(e, g, s));
   // dx = dy + rmsnorm_bwd(x1, ...)   (model.py:259, approx.py:130)
   TRY(rmsnorm_bwd(e, ws, c->x1, lw->norm_ffn, inv2, dh, dy, dx, dx_c, gr->norm_ffn, gr->alpha_ffn, b, m, s));
@@ -605,12 +692,14 @@ int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights*
       g = GemmCall();
       g.M = m; g.N = f; g.K = b;
       g.a = {dy_c, m, false}; g.b = {act, f, false};
+      g.tag = "nbr.wgrad_down";
       TRY(gemm_accumulate(e, g, gr->down, f, gr->alpha_ffn, s));
     }
     if (gr->gu) {  // [g_gate; g_up] = [d_gate | d_up]^T h2 (model.py:255-256)
       g = GemmCall();
       g.M = 2 * f; g.N = m; g.K = b;
       g.a = {dcat, 2 * f, false}; g.b = {h2, m, false};
+      g.tag = "nbr.wgrad_gu";
       TRY(gemm_accumulate(e, g, gr->gu, m, gr->alpha_ffn, s));
     }
   }
@@ -655,23 +744,27 @@ int mecefo_backward_block_exact(mecefo_engine* e, const mecefo_layer_weights* lw
   ep.kind = EPI_SWIGLU_BWD_CACHED; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
   ep.aux = c->gu; ep.ldaux = 2 * f; ep.offaux = f; ep.act_prec = e->prec;
   g.epi = ep;
+  g.tag = "exact.d_act_swiglu_bwd";
   TRY(run_gemm(e, g, s));
   g = GemmCall();
   g.M = b; g.N = m; g.K = 2 * f;
   g.a = {dcat, 2 * f, true}; g.b = {lw->w_gu_c, m, false};
   g.epi = epi_store(dh, m, PREC_F32);
+  g.tag = "exact.d_h2";
   TRY(run_gemm(e, g, s));
   TRY(rmsnorm_bwd(e, ws, c->x1, lw->norm_ffn, c->inv2, dh, dy, dx1, dx1_c, gr->norm_ffn, gr->alpha_ffn, b, m, s));
   if (gr->down) {
     g = GemmCall();
     g.M = m; g.N = f; g.K = b;
     g.a = {dy_c, m, false}; g.b = {c->act, f, false};
+    g.tag = "exact.wgrad_down";
     TRY(gemm_accumulate(e, g, gr->down, f, gr->alpha_ffn, s));
   }
   if (gr->gu) {
     g = GemmCall();
     g.M = 2 * f; g.N = m; g.K = b;
     g.a = {dcat, 2 * f, false}; g.b = {c->h2, m, false};
+    g.tag = "exact.wgrad_gu";
     TRY(gemm_accumulate(e, g, gr->gu, m, gr->alpha_ffn, s));
   }
   // ---- attention sub-block (model.py:336-368) ----
@@ -679,11 +772,13 @@ int mecefo_backward_block_exact(mecefo_engine* e, const mecefo_layer_weights* lw
   g.M = b; g.N = m; g.K = m;
   g.a = {dx1_c, m, true}; g.b = {lw->w_o_c, m, false};
   g.epi = epi_store(dctx, m, e->prec);
+  g.tag = "exact.d_ctx";
   TRY(run_gemm(e, g, s));
   if (gr->o) {  // g_o = dx1^T ctx
     g = GemmCall();
     g.M = m; g.N = m; g.K = b;
     g.a = {dx1_c, m, false}; g.b = {c->ctx, m, false};
+    g.tag = "exact.wgrad_o";
     TRY(gemm_accumulate(e, g, gr->o, m, gr->alpha_mha, s));
   }
   AttnDev a = attn_args(e);
@@ -694,11 +789,13 @@ int mecefo_backward_block_exact(mecefo_engine* e, const mecefo_layer_weights* lw
   g.M = b; g.N = m; g.K = 3 * m;
   g.a = {dqkv, 3 * m, true}; g.b = {lw->w_qkv_c, m, false};
   g.epi = epi_store(dh, m, PREC_F32);
+  g.tag = "exact.d_h1";
   TRY(run_gemm(e, g, s));
   if (gr->qkv) {  // [g_q; g_k; g_v] = d_qkv^T h1
     g = GemmCall();
     g.M = 3 * m; g.N = m; g.K = b;
     g.a = {dqkv, 3 * m, false}; g.b = {c->h1, m, false};
+    g.tag = "exact.wgrad_qkv";
     TRY(gemm_accumulate(e, g, gr->qkv, m, gr->alpha_mha, s));
   }
   // dx = dx1 + rmsnorm_bwd(x, g_mha, inv1, d_h1)   (model.py:433-434)
@@ -725,6 +822,7 @@ int mecefo_recompute_ffn(mecefo_engine* e, const mecefo_layer_weights* lw, const
   Epilogue ep{};
   ep.kind = EPI_SWIGLU_FWD; ep.out = act; ep.ldo = f; ep.out2 = gu; ep.ldo2 = 2 * f; ep.off2 = f; ep.act_prec = e->prec;
   g.epi = ep;
+  g.tag = "recompute.gu";
   TRY(run_gemm(e, g, s));
   if (gu) {
     if (gate) CUDA_TRY(cudaMemcpy2DAsync(gate, f * e->ps, gu, 2 * f * e->ps, f * e->ps, b, cudaMemcpyDeviceToDevice, s));
@@ -737,6 +835,7 @@ int mecefo_recompute_ffn(mecefo_engine* e, const mecefo_layer_weights* lw, const
     g.M = b; g.N = m; g.K = f;
     g.a = {act, f, true}; g.b = {lw->w_down_c, f, true};
     g.epi = epi_store(down, m, PREC_F32);
+    g.tag = "recompute.down";
     TRY(run_gemm(e, g, s));
   }
   return MECEFO_OK;
@@ -760,12 +859,14 @@ int mecefo_lowrank_wgrad(mecefo_engine* e, const void* g_y, const void* x, const
   g.M = batch; g.N = rank; g.K = n_in;
   g.a = {x, batch, false}; g.b = {v1, rank, false};
   g.epi = epi_store(P, rank, e->prec);
+  g.tag = "lowrank_api.P";
   TRY(run_gemm(e, g, s));
   // Q = g_y P (n_out, rank): A = g_y K-major (ld batch), B(n=r, k=b) = P[k, n] MN-major
   CUDA_TRY(cudaMemsetAsync(Q, 0, n_out * rank * 4, s));
   g = GemmCall();
   g.M = n_out; g.N = rank; g.K = batch;
   g.a = {g_y, batch, true}; g.b = {P, rank, false};
+  g.tag = "lowrank_api.Q";
   TRY(gemm_accumulate(e, g, Q, rank, 1.f, s));
   if (e->prec == PREC_BF16) TRY(cast_to_compute(e, Q, Qc, n_out * rank, s));
   // out += alpha Q V1^T: B(n=in, k=r) = v1[n, k] K-major
@@ -773,6 +874,7 @@ int mecefo_lowrank_wgrad(mecefo_engine* e, const void* g_y, const void* x, const
   g.M = n_out; g.N = n_in; g.K = rank;
   g.a = {Qc, rank, true}; g.b = {v1, rank, true};
   g.epi = epi_store(out, n_in, PREC_F32, alpha, 1.f);
+  g.tag = "lowrank_api.up_proj";
   return run_gemm(e, g, s);
 }
 
@@ -793,6 +895,7 @@ int mecefo_head_logits(mecefo_engine* e, const float* x_last, const float* final
   g.M = b; g.N = V; g.K = m;
   g.a = {xf, m, true}; g.b = {unemb_c, m, true};
   g.epi = epi_store(logits, V, e->prec);
+  g.tag = "head.logits";
   return run_gemm(e, g, s);
 }
 
@@ -806,6 +909,7 @@ int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets,
   TRY(ws.take(b * 4, reinterpret_cast<void**>(&rows)));
   TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
+  ProfScope prof("cross_entropy", 0.0, 2.0 * b * V * e->ps, s);
   cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
                                                     bad);
   TRY(check_launch("cross_entropy_kernel"));
@@ -833,12 +937,14 @@ int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* fin
     GemmCall g;
     g.M = V; g.N = m; g.K = b;
     g.a = {dlogits, V, false}; g.b = {xf, m, false};
+    g.tag = "head.g_unemb";
     TRY(gemm_accumulate(e, g, g_unemb, m, alpha, s));
   }
   GemmCall g;  // d_xf = dlogits Wun  (model.py:481)
   g.M = b; g.N = m; g.K = V;
   g.a = {dlogits, V, true}; g.b = {unemb_c, m, false};
   g.epi = epi_store(dxf, m, PREC_F32);
+  g.tag = "head.d_xf";
   TRY(run_gemm(e, g, s));
   return rmsnorm_bwd(e, ws, x_last, final_norm, inv_f, dxf, nullptr, dx, dx_c, g_final, alpha, b, m, s);
 }

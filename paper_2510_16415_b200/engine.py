@@ -1,0 +1,206 @@
+"""Fused MeCeFO training step on one GPU (one process per GPU).
+
+The reference runs every logical DP rank sequentially in one process, keeps
+per-rank gradient dicts and averages them afterwards (harness.py:406-428,
+cluster.py:292-322). Here each process owns persistent HBM buffers and runs
+the microbatches assigned to its GPU by the replicated control plane:
+
+  * activations: the residual stream x_0..x_L and x1_l (fp32) — the whole lean
+    cache — plus full caches only for layers run exactly;
+  * gradients: ONE flat fp32 buffer with the parameter layout. Every backward
+    kernel accumulates g += alpha * dW straight into it, alpha being the
+    Eq. (1) weight 1/|N_{l,#}| of that microbatch (or nothing at all when the
+    microbatch is outside the active set: select, not multiply);
+  * exchange: one NCCL all-reduce(sum) of the flat buffer over NVLink turns the
+    pre-weighted local sums into the Eq. (1) averages on every GPU;
+  * update: one fused multi-tensor AdamW launch with per-parameter step
+    counts and the Eq. (1) skip list, which also refreshes the bf16 shadow.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, approx, model as mdl, optim as op, runtime
+from .linalg import SvdConfig
+
+
+@dataclass
+class Microbatch:
+    """One logical DP rank's work this iteration (harness.py:406-418)."""
+
+    rank: int                 # logical DP rank j
+    tokens: torch.Tensor      # (B, T) int64, device or pinned host
+    targets: torch.Tensor     # (B, T) int64
+    lean: list                # per layer: True -> CACHE_FFN_INPUT_ONLY + neighbor backward
+    alpha_mha: list           # per layer: Eq. (1) weight for MHA grads, or None (not in N_MHA)
+    alpha_ffn: float          # 1/|N_FFN| = 1/R
+    alpha_global: float       # 1/R (global params average over all ranks)
+
+
+class StepEngine:
+    def __init__(self, cfg: mdl.ModelConfig, precision: str = "bf16", seqs_per_microbatch: int = 32, r: int = 128,
+                 tau: int = 100, optim_cfg: op.OptimConfig | None = None, seed: int = 0,
+                 weights: mdl.ModelWeights | None = None, svd: SvdConfig | None = None, svd_budgeted: bool = False,
+                 group=None):
+        runtime.require_cuda()
+        self.cfg = cfg
+        self.precision = precision
+        self.weights = weights if weights is not None else mdl.init_weights(cfg, seed, precision=precision)
+        self.device = self.weights.master.device
+        self.eng = runtime.engine_for(cfg, precision)
+        self.dtype = self.eng.dtype
+        self.seqs = seqs_per_microbatch
+        self.b = seqs_per_microbatch * cfg.seq_len
+        self.r = r
+        self.tau = tau
+        self.svd = svd if svd is not None else SvdConfig(rank=r, tolerance=1e-9, max_iterations=3000, seed=seed + 23)
+        self.svd_budgeted = svd_budgeted
+        self.group = group
+        self.opt = op.OptimState(optim_cfg or op.OptimConfig())
+        self.opt.ensure_flat(self.weights.total, self.device)
+        self.grad = torch.zeros(self.weights.total, dtype=torch.float32, device=self.device)
+        self.lws = [lw.struct() for lw in self.weights.layers]
+        b, m, L = self.b, cfg.hidden, cfg.layers
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.xs = [torch.empty(b, m, **f32) for _ in range(L + 1)]
+        self.x1s = [torch.empty(b, m, **f32) for _ in range(L)]
+        self.full = None
+        self.dx = [torch.empty(b, m, **f32) for _ in range(2)]
+        self.dx_c = [torch.empty(b, m, dtype=self.dtype, device=self.device) for _ in range(2)] \
+            if precision != "fp32" else [None, None]
+        self.xf = torch.empty(b, m, dtype=self.dtype, device=self.device)
+        self.inv_f = torch.empty(b, **f32)
+        self.logits = torch.empty(b, cfg.vocab, dtype=self.dtype, device=self.device)
+        self.tok = torch.empty(b, dtype=torch.int64, device=self.device)
+        self.tgt = torch.empty(b, dtype=torch.int64, device=self.device)
+        self.rp = approx._pad16(r)
+        nbytes = int(_lib.load().mecefo_workspace_bytes(self.eng.handle, b, self.rp))
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.projs: dict = {}
+        self._keep = []
+        self.losses = None
+
+    # ------------------------------------------------------------------ utils
+    def _gp(self, name: str) -> int:
+        return self.grad.data_ptr() + 4 * self.weights.offsets[name]
+
+    def _layer_grads(self, l: int, alpha_mha, alpha_ffn: float) -> _lib.LayerGrads:
+        p = f"layers.{l}."
+        if alpha_mha is None:
+            return _lib.LayerGrads(None, None, None, 0.0, self._gp(p + "gate"), self._gp(p + "down"),
+                                   self._gp(p + "norm_ffn"), alpha_ffn)
+        return _lib.LayerGrads(self._gp(p + "q"), self._gp(p + "o"), self._gp(p + "norm_mha"), alpha_mha,
+                               self._gp(p + "gate"), self._gp(p + "down"), self._gp(p + "norm_ffn"), alpha_ffn)
+
+    def _full_cache(self, l: int) -> dict:
+        if self.full is None:
+            self.full = [None] * self.cfg.layers
+        if self.full[l] is None:
+            self.full[l] = mdl._alloc_full_cache(self.cfg, self.b, self.dtype, self.device)
+        return self.full[l]
+
+    def proj(self, rank: int, layer: int) -> approx.ProjectionCache:
+        key = (rank, layer)
+        if key not in self.projs:
+            self.projs[key] = approx.ProjectionCache(rank=self.r, refresh_period=self.tau)
+        return self.projs[key]
+
+    def reset_projection(self, rank: int, layer: int) -> None:
+        """harness.py:384-388: adopted layers start a fresh basis."""
+        if (rank, layer) in self.projs:
+            self.projs[(rank, layer)].reset()
+
+    # ---------------------------------------------------------- microbatch
+    def microbatch(self, mb: Microbatch, loss_ptr: int) -> None:
+        cfg, eng, b, s = self.cfg, self.eng, self.b, runtime.stream_ptr()
+        w = self.weights
+        ws, wn = self.ws.data_ptr(), self.ws.numel()
+        self.tok.copy_(mb.tokens.reshape(-1), non_blocking=True)
+        self.tgt.copy_(mb.targets.reshape(-1), non_blocking=True)
+        _lib.call("mecefo_embedding_forward", eng.handle, self.tok.data_ptr(),
+                  w.master.data_ptr() + 4 * w.offsets["embedding"], self.xs[0].data_ptr(), b, s)
+        caches = []
+        for l in range(cfg.layers):
+            full = None if mb.lean[l] else self._full_cache(l)
+            cache = mdl.BlockCache(mode=mdl.CACHE_FFN_INPUT_ONLY if mb.lean[l] else mdl.CACHE_FULL,
+                                   x=self.xs[l], x1=self.x1s[l], full=full)
+            cs = cache.struct()
+            caches.append(cs)
+            _lib.call("mecefo_forward_block", eng.handle, ctypes.byref(self.lws[l]), ctypes.byref(cs),
+                      self.xs[l + 1].data_ptr(), None, b,
+                      _lib.CACHE_FFN_INPUT_ONLY if mb.lean[l] else _lib.CACHE_FULL, ws, wn, s)
+        _lib.call("mecefo_head_logits", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
+                  w.shadow_view("unembedding").data_ptr(), b, self.xf.data_ptr(), self.inv_f.data_ptr(),
+                  self.logits.data_ptr(), s)
+        _lib.call("mecefo_cross_entropy", eng.handle, self.logits.data_ptr(), self.tgt.data_ptr(), b, loss_ptr, ws, wn,
+                  s)
+        cur = 0
+        _lib.call("mecefo_head_backward", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
+                  self.inv_f.data_ptr(), self.xf.data_ptr(), self.logits.data_ptr(),
+                  w.shadow_view("unembedding").data_ptr(), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
+                  self._gp("final_norm"), self._gp("unembedding"), mb.alpha_global, b, ws, wn, s)
+        for l in reversed(range(cfg.layers)):
+            nxt = 1 - cur
+            g = self._layer_grads(l, mb.alpha_mha[l], mb.alpha_ffn)
+            if mb.lean[l]:
+                pc = self.proj(mb.rank, l)
+                approx.refresh_projections(pc, w.layers[l], self.svd, budgeted=self.svd_budgeted)
+                pst, keep, rp = pc.packed(self.precision)
+                self._keep = keep
+                _lib.call("mecefo_backward_block_neighbor", eng.handle, ctypes.byref(self.lws[l]),
+                          ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
+                          self.dx[nxt].data_ptr(), runtime.ptr(self.dx_c[nxt]), ctypes.byref(g), ctypes.byref(pst), b,
+                          ws, wn, s)
+                pc.step += 1
+            else:
+                _lib.call("mecefo_backward_block_exact", eng.handle, ctypes.byref(self.lws[l]),
+                          ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
+                          self.dx[nxt].data_ptr(), runtime.ptr(self.dx_c[nxt]), ctypes.byref(g), b, ws, wn, s)
+            cur = nxt
+        _lib.call("mecefo_embedding_backward", eng.handle, self.tok.data_ptr(), self.dx[cur].data_ptr(),
+                  self._gp("embedding"), mb.alpha_global, b, s)
+
+    # ---------------------------------------------------------------- step
+    def step(self, mbs: list, n_ranks: int, lr: float, skip=(), check: bool = True) -> torch.Tensor:
+        """Run this GPU's microbatches, exchange, update. Returns the (n_ranks,)
+        device vector of per-rank losses (all-reduced across processes)."""
+        self.grad.zero_()
+        losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
+        for mb in mbs:
+            self.microbatch(mb, losses.data_ptr() + 4 * mb.rank)
+        if self.group is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=self.group)
+        op.apply_flat(self.weights, self.opt, self.grad, lr, skip=skip, check=check)
+        self.losses = losses
+        return losses
+
+
+def ring_plan(n_ranks: int, failed, layers: int, gpu_of_rank=None):
+    """Flavour-B plan: R logical DP ranks on a ring; a failed
+    rank's microbatch goes to its ring successor (cluster.ring_route), which
+    then runs BOTH microbatches lean on all layers (harness.py:395 predicate
+    at microbatch granularity). Returns (executor, lean_by_rank, alpha_mha,
+    skip) where alpha_mha[l] is 1/|N_MHA| (N_MHA = ranks run exactly) and
+    skip lists the MHA parameters whose active set is empty."""
+    from . import cluster as cl
+    from .errors import UnrecoverableRankError
+
+    route = cl.ring_route(n_ranks, failed)
+    if route is None:
+        raise UnrecoverableRankError(f"ring of {n_ranks}: failed ranks {sorted(failed)} leave no adopter")
+    doubled = {route[j] for j in failed}
+    lean = [route[j] in doubled for j in range(n_ranks)]
+    exact = [j for j in range(n_ranks) if not lean[j]]
+    alpha_mha = (1.0 / len(exact)) if exact else None
+    skip = []
+    if not exact:
+        skip = [f"layers.{l}.{k}" for l in range(layers) for k in ("q", "k", "v", "o", "norm_mha")]
+    return route, lean, alpha_mha, skip
