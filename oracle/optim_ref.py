@@ -41,7 +41,7 @@ class Adam:
 def lr_at(step: int, total: int, base: float, floor_fraction: float = 0.1) -> float:
     warm = math.ceil(0.1 * total)
     if step <= warm:
-        return base * step / warm if warm > 0 else base
+        return base * (step / warm) if warm > 0 else base
     prog = (step - warm) / (total - warm)
     lo = floor_fraction * base
     return lo + (base - lo) * 0.5 * (1.0 + math.cos(math.pi * prog))
