@@ -270,7 +270,10 @@ def main():
         eng.step(degraded, R, lr, skip=skip_d, check=False)
     torch.cuda.synchronize()
     if args.profile_only:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off captures only the timed steps
         ms, _, _ = timed(degraded, skip_d, args.steps)
+        torch.cuda.cudart().cudaProfilerStop()
         if rank == 0:
             print(json.dumps({"profile_only": True, "ms_per_step": ms / args.steps}), flush=True)
         return

@@ -1,11 +1,13 @@
-// Causal multi-head attention with interleaved-pair RoPE (model.py:268-368).
+// Causal multi-head attention (model.py:317-368), SIMT fp32 path (fp32 parity
+// mode, head dims != 64, and the exact backward).
 //
-// Forward keeps only the per-row log-sum-exp (no (B,H,T,T) probabilities, the
-// lean forward of approx.py needs none of them); backward recomputes scores
-// from q/k and the saved LSE. One CTA per (sequence, head, 64-query block);
-// each query row is owned by 4 threads that split the key loop and merge
-// their online-softmax states with warp shuffles. K/V (or Q/dO for the
-// key-side backward) are staged once per CTA in shared memory, rotated.
+// q and k arrive already RoPE-rotated: the QKV GEMM epilogue applies the
+// interleaved-pair rotation (model.py:281-288), exactly what the reference's
+// full cache stores. The backward applies the transpose rotation to dq/dk
+// (model.py:291-298). Forward keeps only the per-row log-sum-exp; backward
+// recomputes scores. One CTA per (sequence, head, 64-query block); each query
+// row is owned by 4 threads that split the key loop and merge their
+// online-softmax states with warp shuffles.
 #pragma once
 #include "common.cuh"
 
@@ -67,16 +69,13 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(AttnDev a) {
   float* Ks = sm;
   float* Vs = sm + (size_t)kend * (D + 4);
   const int64_t row_base = (int64_t)seq * a.T;
-  stage_rows<D>(Ks, a.qkv, a.ld_qkv, row_base, a.m + h * D, 0, kend, a, true, 1.f);
+  stage_rows<D>(Ks, a.qkv, a.ld_qkv, row_base, a.m + h * D, 0, kend, a, false, 1.f);
   stage_rows<D>(Vs, a.qkv, a.ld_qkv, row_base, 2 * a.m + h * D, 0, kend, a, false, 1.f);
   __syncthreads();
   const int i = q0 + (threadIdx.x >> 2), sl = threadIdx.x & 3;
   const bool valid = i < a.T;
   float q[D], o[D];
-  if (valid) {
-    load_head_row<D>(a.qkv, (row_base + i) * a.ld_qkv + h * D, q, a.prec);
-    rope_rotate<D>(q, a, i, 1.f);
-  }
+  if (valid) load_head_row<D>(a.qkv, (row_base + i) * a.ld_qkv + h * D, q, a.prec);
 #pragma unroll
   for (int c = 0; c < D; ++c) { q[c] = valid ? q[c] * a.scale : 0.f; o[c] = 0.f; }
   float mx = -INFINITY, l = 0.f;
@@ -133,14 +132,13 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(AttnDev a) {
   float* Ks = sm;
   float* Vs = sm + (size_t)kend * (D + 4);
   const int64_t row_base = (int64_t)seq * a.T;
-  stage_rows<D>(Ks, a.qkv, a.ld_qkv, row_base, a.m + h * D, 0, kend, a, true, 1.f);
+  stage_rows<D>(Ks, a.qkv, a.ld_qkv, row_base, a.m + h * D, 0, kend, a, false, 1.f);
   stage_rows<D>(Vs, a.qkv, a.ld_qkv, row_base, 2 * a.m + h * D, 0, kend, a, false, 1.f);
   __syncthreads();
   const int i = q0 + (threadIdx.x >> 2), sl = threadIdx.x & 3;
   if (i >= a.T) return;  // whole 4-lane groups exit together; no shuffles below cross groups
   float q[D], dO[D], dq[D];
   load_head_row<D>(a.qkv, (row_base + i) * a.ld_qkv + h * D, q, a.prec);
-  rope_rotate<D>(q, a, i, 1.f);
   load_head_row<D>(a.dctx, (row_base + i) * a.ld_ctx + h * D, dO, a.prec);
   float Dsum = 0.f;
   {
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dkv_kernel(AttnDev a) {
   float* Ls = Os + (size_t)nq * (D + 4);
   float* Ds = Ls + nq;
   const int64_t row_base = (int64_t)seq * a.T;
-  stage_rows<D>(Qs, a.qkv, a.ld_qkv, row_base, h * D, k0, a.T, a, true, a.scale);
+  stage_rows<D>(Qs, a.qkv, a.ld_qkv, row_base, h * D, k0, a.T, a, false, a.scale);
   stage_rows<D>(Os, a.dctx, a.ld_ctx, row_base, h * D, k0, a.T, a, false, 1.f);
   for (int r = threadIdx.x; r < nq; r += blockDim.x) {
     Ls[r] = a.lse[(row_base + k0 + r) * a.H + h];
@@ -203,7 +201,6 @@ __global__ void __launch_bounds__(256) attn_bwd_dkv_kernel(AttnDev a) {
   if (j >= a.T) return;
   float k[D], v[D], dk[D], dv[D];
   load_head_row<D>(a.qkv, (row_base + j) * a.ld_qkv + a.m + h * D, k, a.prec);
-  rope_rotate<D>(k, a, j, 1.f);
   load_head_row<D>(a.qkv, (row_base + j) * a.ld_qkv + 2 * a.m + h * D, v, a.prec);
 #pragma unroll
   for (int c = 0; c < D; ++c) { dk[c] = 0.f; dv[c] = 0.f; }

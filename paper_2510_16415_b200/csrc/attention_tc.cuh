@@ -1,0 +1,160 @@
+// Tensor-core causal attention forward for head_dim 64 and T <= 256 (bf16).
+//
+// One CTA per (sequence, head, 128-query block). Because a whole causal key
+// range (<= 256 keys) fits one tcgen05 accumulator (M=128, N<=256 fp32 columns
+// of TMEM), the softmax is exact and single-pass — no online rescaling:
+//   1. TMA: Q block (128x64), K and V rows [0, nk) (nk <= 256) -> smem (SW128)
+//   2. tcgen05.mma  S = Q K^T            -> TMEM cols [0, nk)
+//   3. 4 warps (one query row per thread): row max, p = exp(scale (s - max)),
+//      causal mask, row sum; P (bf16) -> smem in the UMMA K-major SW128 layout
+//   4. tcgen05.mma  O = P V (V as an MN-major B operand) -> TMEM cols [256,320)
+//   5. O / rowsum -> ctx (bf16), LSE (full cache only)
+// q/k arrive RoPE-rotated from the QKV GEMM epilogue (model.py:281-288,
+// 323-331). The (B,H,T,T) probabilities never touch HBM.
+#pragma once
+#include "gemm.cuh"
+
+namespace mecefo {
+
+struct AttnTcArgs {
+  void* ctx;
+  int64_t ld_ctx;
+  float* lse;
+  int T, H, m;
+  float scale;
+};
+
+constexpr int ATC_THREADS = 128;
+constexpr int ATC_SMEM = 16384 + 32768 + 32768 + 65536 + 1024 + 256;
+
+__global__ void __launch_bounds__(ATC_THREADS, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, AttnTcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + 16384;
+  uint8_t* sV = sK + 32768;
+  uint8_t* sP = sV + 32768;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 65536);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seq = blockIdx.x / a.H, h = blockIdx.x % a.H;
+  const int q0 = blockIdx.y * 128;
+  const int nk = min(a.T, q0 + 128);   // keys 0..nk-1 (multiple of 64)
+  const int nq = min(128, a.T - q0);   // valid query rows in this block
+  const int row0 = seq * a.T;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bars[0], 16384 + 2 * nk * 128);
+    tma_load_2d(sQ, &tq, &bars[0], h * 64, row0 + q0);
+    tma_load_2d(sQ + 8192, &tq, &bars[0], h * 64, row0 + q0 + 64);
+    for (int kb = 0; kb < nk / 64; ++kb) {
+      tma_load_2d(sK + kb * 8192, &tq, &bars[0], a.m + h * 64, row0 + kb * 64);
+      tma_load_2d(sV + kb * 8192, &tq, &bars[0], 2 * a.m + h * 64, row0 + kb * 64);
+    }
+    mbar_wait(&bars[0], 0);
+    tc_fence_after();
+    // S = Q K^T: A, B K-major; M = 128, N = nk, K = 64
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nk >> 3) << 17) | ((128u >> 4) << 24);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      tc_mma_bf16(tmem, make_sdesc(smem_u32(sQ) + k * 32, 16, 1024), make_sdesc(smem_u32(sK) + k * 32, 16, 1024),
+                  idesc, k > 0 ? 1u : 0u);
+    tc_commit(&bars[1]);
+  }
+  mbar_wait(&bars[1], 0);
+  tc_fence_after();
+
+  const int row = warp * 32 + lane;
+  const int qi = q0 + row;  // query position in the sequence
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  const float c2 = a.scale * 1.4426950408889634f;
+  float mx = -INFINITY;
+  for (int c = 0; c < nk / 16; ++c) {
+    float v[16];
+    tmem_ld16(taddr + c * 16, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c * 16 + j <= qi) mx = fmaxf(mx, v[j]);
+  }
+  const bool valid = row < nq;
+  float l = 0.f;
+  for (int c = 0; c < nk / 16; ++c) {
+    float v[16];
+    tmem_ld16(taddr + c * 16, v);
+    uint32_t pk[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k0 = c * 16 + 2 * j;
+      const float p0 = (valid && k0 <= qi) ? exp2f((v[2 * j] - mx) * c2) : 0.f;
+      const float p1 = (valid && k0 + 1 <= qi) ? exp2f((v[2 * j + 1] - mx) * c2) : 0.f;
+      __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
+      // the row sum uses the bf16-rounded probabilities that feed P V
+      const float2 back = __bfloat1622float2(hp);
+      l += back.x + back.y;
+      pk[j] = *reinterpret_cast<uint32_t*>(&hp);
+    }
+    // P row `row`, keys [16c, 16c+16): 64-key block c/4, bytes (c%4)*32 .. +32 of the 128-B row
+    uint8_t* blk = sP + (c >> 2) * 16384 + row * 128;
+    const int u0 = (c & 3) * 2;
+    *reinterpret_cast<uint4*>(blk + (((u0) ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    *reinterpret_cast<uint4*>(blk + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    // O = P V: A = P K-major (K = keys), B = V MN-major (N = d = 64)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+    for (int s = 0; s < nk / 16; ++s)
+      tc_mma_bf16(tmem + 256, make_sdesc(smem_u32(sP) + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
+                  make_sdesc(smem_u32(sV) + s * 2048, 8192, 1024), idesc, s > 0 ? 1u : 0u);
+    tc_commit(&bars[2]);
+  }
+  mbar_wait(&bars[2], 0);
+  tc_fence_after();
+  const float il = 1.f / l;
+  uint32_t ow[32];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float v[16];
+    tmem_ld16(taddr + 256 + c * 16, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      __nv_bfloat162 hp = __floats2bfloat162_rn(v[2 * j] * il, v[2 * j + 1] * il);
+      ow[c * 8 + j] = *reinterpret_cast<uint32_t*>(&hp);
+    }
+  }
+  if (valid) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.ctx) + (int64_t)(row0 + qi) * a.ld_ctx +
+                                          h * 64);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dst[u] = make_uint4(ow[4 * u], ow[4 * u + 1], ow[4 * u + 2], ow[4 * u + 3]);
+    if (a.lse) a.lse[(int64_t)(row0 + qi) * a.H + h] = mx * a.scale + logf(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+  }
+}
+
+}  // namespace mecefo

@@ -15,6 +15,7 @@
 
 #include "../../include/mecefo.h"
 #include "attention.cuh"
+#include "attention_tc.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -358,9 +359,23 @@ int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cu
 }
 
 int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaStream_t s) {
+  const int hd = (int)(e->d.hidden / e->d.heads);
+  if (!backward && e->prec == PREC_BF16 && hd == 64 && a.T % 64 == 0 && a.T <= 256) {
+    ProfScope prof("attn_fwd_tc", 2.0 * tokens * a.T * a.m, (double)tokens * a.m * e->ps * 4, s);
+    CUtensorMap tq;
+    TRY(make_tmap(e, &tq, a.qkv, 3 * a.m, tokens, a.ld_qkv, 64, 64));
+    AttnTcArgs t{a.ctx, a.ld_ctx, a.lse, a.T, a.H, a.m, a.scale};
+    static bool set = false;
+    if (!set) {
+      CUDA_TRY(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATC_SMEM));
+      set = true;
+    }
+    dim3 grid((unsigned)(tokens / a.T) * a.H, (unsigned)((a.T + 127) / 128));
+    attn_fwd_tc_kernel<<<grid, ATC_THREADS, ATC_SMEM, s>>>(tq, t);
+    return check_launch("attn_fwd_tc_kernel");
+  }
   ProfScope prof(backward ? "attn_bwd" : "attn_fwd", (backward ? 4.0 : 2.0) * tokens * a.T * a.m,
                  (double)tokens * a.m * e->ps * (backward ? 9 : 4), s);
-  const int hd = (int)(e->d.hidden / e->d.heads);
   const int nseq = (int)(tokens / e->d.seq_len);
   dim3 grid(nseq * a.H, (a.T + 63) / 64);
   const size_t per_row = (size_t)(hd + 4) * sizeof(float);
@@ -536,6 +551,10 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   g.M = b; g.N = 3 * m; g.K = m;
   g.a = {h1, m, true}; g.b = {lw->w_qkv_c, m, true};
   g.epi = epi_store(qkv, 3 * m, e->prec);
+  if (e->d.rope) {  // q, k leave the GEMM rotated (model.py:323-326)
+    g.epi.rope_cos = e->rope_cos; g.epi.rope_sin = e->rope_sin;
+    g.epi.rope_T = (int)e->d.seq_len; g.epi.rope_hd = (int)(m / e->d.heads); g.epi.rope_cols = (int)(2 * m);
+  }
   g.tag = "fwd.qkv";
   TRY(run_gemm(e, g, s));
   // causal attention with RoPE -> ctx                         (model.py:323-331)

@@ -45,6 +45,11 @@ struct Epilogue {
   int64_t ldaux;
   int64_t offaux;
   int act_prec;
+  // RoPE on the q|k columns [0, rope_cols) of a QKV projection (model.py:281-288):
+  // interleaved (even, odd) pairs rotated by pos * theta_j, pos = row % rope_T.
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_T, rope_hd, rope_cols;
 };
 
 struct GemmDev {
@@ -131,6 +136,20 @@ __device__ __forceinline__ void epi_apply(const Epilogue& e, int r, int n0, int 
     const int64_t idx = (int64_t)r * e.ldo + n0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] *= e.alpha;
+    if (e.rope_cos && n0 < e.rope_cols) {
+      const int pos = r % e.rope_T, half = e.rope_hd >> 1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = n0 + 2 * j;
+        if (c < e.rope_cols) {
+          const int pi = pos * half + ((c % e.rope_hd) >> 1);
+          const float cs = e.rope_cos[pi], sn = e.rope_sin[pi];
+          const float ev = v[2 * j], od = v[2 * j + 1];
+          v[2 * j] = ev * cs - od * sn;
+          v[2 * j + 1] = ev * sn + od * cs;
+        }
+      }
+    }
     if (e.beta != 0.f) {
       float o[16];
       load16(e.out, idx, o, cnt, PREC_F32);

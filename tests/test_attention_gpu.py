@@ -1,0 +1,81 @@
+"""GPU: head_dim-64 / T=256 block (the LLaMA-60M..1B attention shape) against
+the float64 oracle — exercises the tcgen05 attention forward (bf16), the RoPE
+GEMM epilogue and the SIMT exact backward on pre-rotated q/k."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import model_ref as R
+from paper_2510_16415_b200 import approx, model as mdl
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 5e-2
+
+
+def _setup(hidden=512, heads=8, ffn=1376, T=256, seqs=2, seed=0):
+    cfg = mdl.ModelConfig(vocab=64, hidden=hidden, heads=heads, ffn_intermediate=ffn, layers=1, seq_len=T)
+    d = R.Dims(64, hidden, heads, ffn, 1, T)
+    W = R.init_params(d, seed)
+    rng = np.random.Generator(np.random.PCG64(seed + 1))
+    x = rng.normal(size=(seqs * T, hidden)) * 0.5
+    dy = rng.normal(size=(seqs * T, hidden)) * 0.01
+    return cfg, d, W, x, dy
+
+
+@pytest.mark.parametrize("prec,tol", [("bf16", BF16_TOL), ("fp32", 1e-4)])
+@pytest.mark.parametrize("T,seqs", [(256, 2), (128, 3), (192, 2)])
+def test_forward_block_hd64(cuda, prec, tol, T, seqs):
+    cfg, d, W, x, dy = _setup(T=T, seqs=seqs)
+    y_ref, c_ref = R.block_fwd(d, W, 0, x.reshape(seqs, T, -1), lean=False)
+    w = mdl.init_weights(cfg, 0, precision=prec)
+    xt = torch.tensor(x, dtype=torch.float32, device="cuda")
+    y, cache = mdl.forward_block(cfg, w.layers[0], xt, mdl.CACHE_FULL)
+    assert R.rel_err(y.cpu().numpy(), y_ref.reshape(x.shape)) < tol
+    assert R.rel_err(cache.x1.cpu().numpy(), c_ref["x1"].reshape(x.shape)) < tol
+    # cached q/k are post-RoPE, like the reference's full cache (model.py:323-326)
+    q_ref = R.heads_merge(c_ref["attn"]["q"]).reshape(x.shape)
+    k_ref = R.heads_merge(c_ref["attn"]["k"]).reshape(x.shape)
+    qkv = cache.full["qkv"].float().cpu().numpy()
+    assert R.rel_err(qkv[:, :512], q_ref) < tol
+    assert R.rel_err(qkv[:, 512:1024], k_ref) < tol
+    assert R.rel_err(cache.full["ctx"].float().cpu().numpy(), c_ref["attn"]["ctx"].reshape(x.shape)) < tol
+    # lean forward gives the identical output (model.py:398-418)
+    y2, lean = mdl.forward_block(cfg, w.layers[0], xt, mdl.CACHE_FFN_INPUT_ONLY)
+    assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("prec,tol", [("bf16", BF16_TOL), ("fp32", 1e-4)])
+def test_exact_backward_hd64(cuda, prec, tol):
+    cfg, d, W, x, dy = _setup(seqs=2)
+    _, c_ref = R.block_fwd(d, W, 0, x.reshape(2, 256, -1), lean=False)
+    dx_ref, g_ref = R.block_bwd_exact(d, W, 0, c_ref, dy.reshape(2, 256, -1))
+    w = mdl.init_weights(cfg, 0, precision=prec)
+    _, cache = mdl.forward_block(cfg, w.layers[0], torch.tensor(x, dtype=torch.float32, device="cuda"),
+                                 mdl.CACHE_FULL)
+    dx, g = mdl.backward_block_exact(cfg, w.layers[0], cache, torch.tensor(dy, dtype=torch.float32, device="cuda"))
+    assert R.rel_err(dx.cpu().numpy(), dx_ref.reshape(x.shape)) < tol
+    for k in g:
+        assert R.rel_err(g[k].cpu().numpy(), g_ref[k]) < tol, k
+
+
+def test_lean_backward_hd64_lowrank_r128(cuda):
+    cfg, d, W, x, dy = _setup(seqs=2)
+    rng = np.random.Generator(np.random.PCG64(9))
+    basis = {k: np.linalg.qr(rng.normal(size=(n, 128)))[0] for k, n in (("gate", 512), ("up", 512), ("down", 1376))}
+    _, lean_ref = R.block_fwd(d, W, 0, x.reshape(2, 256, -1), lean=True)
+    dx_ref, g_ref = R.block_bwd_neighbor(d, W, 0, lean_ref, dy.reshape(2, 256, -1), basis)
+    w = mdl.init_weights(cfg, 0, precision="bf16")
+    _, cache = mdl.forward_block(cfg, w.layers[0], torch.tensor(x, dtype=torch.float32, device="cuda"),
+                                 mdl.CACHE_FFN_INPUT_ONLY)
+    proj = approx.ProjectionCache(rank=128, refresh_period=10**9, step=1)
+    for k, v in basis.items():
+        proj.set_basis(k, v)
+    from paper_2510_16415_b200.linalg import SvdConfig
+    dx, g = approx.backward_block_neighbor(cfg, w.layers[0], cache,
+                                           torch.tensor(dy, dtype=torch.float32, device="cuda"), proj=proj,
+                                           svd=SvdConfig(rank=128))
+    assert R.rel_err(dx.cpu().numpy(), dx_ref.reshape(x.shape)) < BF16_TOL
+    for k in g:
+        assert R.rel_err(g[k].cpu().numpy(), g_ref[k]) < BF16_TOL, k
