@@ -40,19 +40,21 @@ def lowrank_wgrad(g_y: torch.Tensor, x: torch.Tensor, v1: torch.Tensor, precisio
     cfg = mdl.ModelConfig(vocab=8, hidden=8, heads=1, ffn_intermediate=8, layers=1, seq_len=1)
     eng = runtime.engine_for(cfg, precision)
     dt = eng.dtype
-    # Zero-pad the batch and rank dims to 16-byte rows (exact: zeros add nothing).
-    bp, rp = (b + 7) // 8 * 8, (r + 7) // 8 * 8
-    gp = torch.zeros(n_out, bp, dtype=dt, device="cuda")
-    xp = torch.zeros(n_in, bp, dtype=dt, device="cuda")
-    vp = torch.zeros(n_in, rp, dtype=dt, device="cuda")
-    gp[:, :b] = g_y.to("cuda", dt)
-    xp[:, :b] = x.to("cuda", dt)
-    vp[:, :r] = v1.to("cuda", dt)
-    out = torch.zeros(n_out, n_in, dtype=torch.float32, device="cuda")
-    ws, wn = eng.workspace(max(bp, n_out, n_in), _pad16(rp))
-    _lib.call("mecefo_lowrank_wgrad", eng.handle, gp.data_ptr(), xp.data_ptr(), vp.data_ptr(), out.data_ptr(), n_out,
-              n_in, bp, rp, 1.0, ws, wn, runtime.stream_ptr())
-    return out
+    # Zero-pad every dim to 16-byte rows for TMA (exact: zero rows/columns
+    # contribute nothing and the padded output block is sliced away).
+    p8 = lambda n: (n + 7) // 8 * 8
+    bp, rp, op_, ip = p8(b), p8(r), p8(n_out), p8(n_in)
+    gp = torch.zeros(op_, bp, dtype=dt, device="cuda")
+    xp = torch.zeros(ip, bp, dtype=dt, device="cuda")
+    vp = torch.zeros(ip, rp, dtype=dt, device="cuda")
+    gp[:n_out, :b] = g_y.to("cuda", dt)
+    xp[:n_in, :b] = x.to("cuda", dt)
+    vp[:n_in, :r] = v1.to("cuda", dt)
+    out = torch.zeros(op_, ip, dtype=torch.float32, device="cuda")
+    ws, wn = eng.workspace(max(bp, op_, ip), _pad16(rp))
+    _lib.call("mecefo_lowrank_wgrad", eng.handle, gp.data_ptr(), xp.data_ptr(), vp.data_ptr(), out.data_ptr(), op_,
+              ip, bp, rp, 1.0, ws, wn, runtime.stream_ptr())
+    return out[:n_out, :n_in].contiguous()
 
 
 @dataclass

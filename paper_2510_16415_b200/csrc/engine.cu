@@ -162,8 +162,8 @@ struct mecefo_engine {
 namespace {
 
 int make_tmap(mecefo_engine* e, CUtensorMap* out, const void* p, int64_t inner, int64_t outer, int64_t ld, int box0,
-              int box1) {
-  TmKey key{p, inner, outer, ld, box0, box1};
+              int box1, int fp32 = 0, int swz = 128) {
+  TmKey key{p, inner, outer, ld, box0, box1 + (fp32 << 20) + (swz << 21)};
   {
     std::lock_guard<std::mutex> lk(e->mu);
     auto it = e->tmaps.find(key);
@@ -173,16 +173,20 @@ int make_tmap(mecefo_engine* e, CUtensorMap* out, const void* p, int64_t inner, 
   if (!enc) return set_err(MECEFO_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   if ((reinterpret_cast<uintptr_t>(p) & 15) != 0)
     return set_err(MECEFO_ERR_CONTRACT, "bf16 GEMM operand %p is not 16-byte aligned", p);
-  if ((ld * 2) % 16 != 0)
-    return set_err(MECEFO_ERR_CONTRACT, "bf16 GEMM operand leading dimension %lld not a multiple of 8 elements",
-                   (long long)ld);
+  const int esz = fp32 ? 4 : 2;
+  if ((ld * esz) % 16 != 0)
+    return set_err(MECEFO_ERR_CONTRACT, "TMA operand leading dimension %lld x %d B is not a multiple of 16 bytes",
+                   (long long)ld, esz);
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
   cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapSwizzle sw = swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swz == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc(out, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(p), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_err(MECEFO_ERR_CONTRACT, "cuTensorMapEncodeTiled failed (%d) for %lldx%lld ld %lld box %dx%d", (int)r,
                    (long long)inner, (long long)outer, (long long)ld, box0, box1);
@@ -239,13 +243,50 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   p.tiles_n = (int)((g.N + cols_per_tile - 1) / cols_per_tile);
   p.num_tiles = p.tiles_m * p.tiles_n * p.split;
   p.epi = g.epi;
+  // output slots -> TMA store / reduce-add maps (32 x 32 boxes, swizzled)
+  TcOut outs{};
+  CUtensorMap to[3];
+  std::memset(to, 0, sizeof(to));
+  const Epilogue& ep = g.epi;
+  struct Slot { void* ptr; int64_t ld; int prec; int reduce; };
+  Slot slots[3] = {{nullptr, 0, 0, 0}, {nullptr, 0, 0, 0}, {nullptr, 0, 0, 0}};
+  const int ps = ep.act_prec == PREC_BF16 ? 2 : 4;
+  switch (ep.kind) {
+    case EPI_STORE:
+      if (ep.beta != 0.f && (ep.beta != 1.f || ep.residual || ep.out_prec != PREC_F32))
+        return set_err(MECEFO_ERR_CONTRACT, "tcgen05 epilogue supports beta in {0,1} (fp32 accumulate) only");
+      slots[0] = {ep.out, ep.ldo, ep.out_prec, ep.beta != 0.f ? 1 : 0};
+      break;
+    case EPI_ATOMIC:
+      slots[0] = {ep.out, ep.ldo, PREC_F32, 1};
+      break;
+    case EPI_SWIGLU_FWD:
+    case EPI_SWIGLU_BWD_RECOMP:
+    case EPI_SWIGLU_BWD_CACHED:
+      if (ep.kind != EPI_SWIGLU_BWD_CACHED && ep.out) slots[0] = {ep.out, ep.ldo, ep.act_prec, 0};
+      if (ep.out2) {
+        slots[1] = {ep.out2, ep.ldo2, ep.act_prec, 0};
+        slots[2] = {reinterpret_cast<uint8_t*>(ep.out2) + ep.off2 * ps, ep.ldo2, ep.act_prec, 0};
+      }
+      break;
+    default:
+      return set_err(MECEFO_ERR_CONSISTENCY, "unknown epilogue kind %d", ep.kind);
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (!slots[k].ptr) continue;
+    const int f32 = slots[k].prec == PREC_F32 ? 1 : 0;
+    TRY(make_tmap(e, &to[k], slots[k].ptr, g.N, g.M, slots[k].ld, 32, 32, f32, f32 ? 128 : 64));
+    outs.used[k] = 1;
+    outs.prec[k] = slots[k].prec;
+    outs.reduce[k] = slots[k].reduce;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<BN, AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const int grid = std::min(p.num_tiles, kNumSMs);
-  gemm_tc_kernel<BN, AK, BKM><<<grid, TC_THREADS, C::SMEM, s>>>(ta, tb, p);
+  gemm_tc_kernel<BN, AK, BKM><<<grid, TC_THREADS, C::SMEM, s>>>(ta, tb, to[0], to[1], to[2], p, outs);
   return check_launch("gemm_tc_kernel");
 }
 
@@ -320,13 +361,42 @@ int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float
   return run_gemm(e, g, s);
 }
 
+template <int NV>
+int launch_rms_fwd(const float* x, const float* g, void* out, float* inv, int64_t rows, int64_t m, int prec,
+                   cudaStream_t s) {
+  rmsnorm_fwd_vec_kernel<NV><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(x, g, out, inv, (int)rows, (int)m, prec);
+  return check_launch("rmsnorm_fwd_vec_kernel");
+}
+
 int rmsnorm_fwd(mecefo_engine* e, const float* x, const float* g, void* out, float* inv, int64_t rows, int64_t m,
                 cudaStream_t s) {
   ProfScope prof("rmsnorm_fwd", 0.0, (double)rows * m * (4 + e->ps) + 4.0 * rows, s);
+  if (m % 4 == 0 && m <= 2048) {
+    const int nv = (int)((m + 127) / 128);
+    if (nv <= 1) return launch_rms_fwd<1>(x, g, out, inv, rows, m, e->prec, s);
+    if (nv <= 2) return launch_rms_fwd<2>(x, g, out, inv, rows, m, e->prec, s);
+    if (nv <= 4) return launch_rms_fwd<4>(x, g, out, inv, rows, m, e->prec, s);
+    if (nv <= 8) return launch_rms_fwd<8>(x, g, out, inv, rows, m, e->prec, s);
+    return launch_rms_fwd<16>(x, g, out, inv, rows, m, e->prec, s);
+  }
   const int warps = 8;
   rmsnorm_fwd_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(x, g, out, inv, (int)rows, (int)m,
                                                                                     e->prec);
   return check_launch("rmsnorm_fwd_kernel");
+}
+
+template <int NV>
+int launch_rms_bwd(const float* x, const float* g, const float* inv, const float* d, const float* resid, float* dx,
+                   void* dx_lp, int prec, float* partial, int64_t rows, int64_t m, int nblk, int rpb, cudaStream_t s) {
+  const int sm = 8 * NV * 32 * 16;
+  static bool set = false;
+  if (!set && sm > 48 * 1024) {
+    CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_vec_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    set = true;
+  }
+  rmsnorm_bwd_vec_kernel<NV><<<nblk, 256, sm, s>>>(x, g, inv, d, resid, dx, dx_lp, prec, partial, (int)rows, (int)m,
+                                                   rpb);
+  return check_launch("rmsnorm_bwd_vec_kernel");
 }
 
 // dx = resid + rmsnorm_bwd(...); grad_scale (+)= alpha * dscale (if non-null).
@@ -334,17 +404,37 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
                 const float* resid, float* dx, void* dx_lp, float* grad_scale, float alpha, int64_t rows, int64_t m,
                 cudaStream_t s) {
   ProfScope prof("rmsnorm_bwd", 0.0, (double)rows * m * (12 + (resid ? 4 : 0) + 4 + (dx_lp ? e->ps : 0)), s);
-  const int rpb = 64;
-  const int nblk = (int)((rows + rpb - 1) / rpb);
+  const bool vec = m % 4 == 0 && m <= 2048;
+  int nblk, rpb;
+  if (vec) {
+    nblk = (int)std::min<int64_t>((rows + 7) / 8, 2 * kNumSMs);
+    rpb = (int)((rows + nblk - 1) / nblk);
+    rpb = (rpb + 7) / 8 * 8;
+    nblk = (int)((rows + rpb - 1) / rpb);
+  } else {
+    rpb = 64;
+    nblk = (int)((rows + rpb - 1) / rpb);
+  }
   float* partial = nullptr;
   if (grad_scale) TRY(ws.take((size_t)nblk * m * sizeof(float), reinterpret_cast<void**>(&partial)));
-  const size_t sm = 8 * m * sizeof(float);
-  if (sm > 48 * 1024) {
-    static bool set = false;
-    if (!set) { CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); set = true; }
+  if (vec) {
+    const int nv = (int)((m + 127) / 128);
+    int rc;
+    if (nv <= 1) rc = launch_rms_bwd<1>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, rows, m, nblk, rpb, s);
+    else if (nv <= 2) rc = launch_rms_bwd<2>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, rows, m, nblk, rpb, s);
+    else if (nv <= 4) rc = launch_rms_bwd<4>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, rows, m, nblk, rpb, s);
+    else if (nv <= 8) rc = launch_rms_bwd<8>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, rows, m, nblk, rpb, s);
+    else rc = launch_rms_bwd<16>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, rows, m, nblk, rpb, s);
+    TRY(rc);
+  } else {
+    const size_t sm = 8 * m * sizeof(float);
+    if (sm > 48 * 1024) {
+      static bool set = false;
+      if (!set) { CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); set = true; }
+    }
+    rmsnorm_bwd_kernel<<<nblk, 256, sm, s>>>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, (int)rows, (int)m, rpb);
+    TRY(check_launch("rmsnorm_bwd_kernel"));
   }
-  rmsnorm_bwd_kernel<<<nblk, 256, sm, s>>>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, (int)rows, (int)m, rpb);
-  TRY(check_launch("rmsnorm_bwd_kernel"));
   if (grad_scale) {
     colsum_finalize_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(partial, nblk, (int)m, grad_scale, alpha, 1.f);
     TRY(check_launch("colsum_finalize_kernel"));
@@ -929,9 +1019,19 @@ int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets,
   TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
   ProfScope prof("cross_entropy", 0.0, 2.0 * b * V * e->ps, s);
-  cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
-                                                    bad);
-  TRY(check_launch("cross_entropy_kernel"));
+  const int nv = (int)((V + 512 * 8 - 1) / (512 * 8));
+  auto* lg = reinterpret_cast<__nv_bfloat16*>(logits);
+  if (e->prec == PREC_BF16 && V % 8 == 0 && nv <= 16) {
+    if (nv <= 2) cross_entropy_bf16_kernel<2><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
+    else if (nv <= 4) cross_entropy_bf16_kernel<4><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
+    else if (nv <= 8) cross_entropy_bf16_kernel<8><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
+    else cross_entropy_bf16_kernel<16><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
+    TRY(check_launch("cross_entropy_bf16_kernel"));
+  } else {
+    cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
+                                                      bad);
+    TRY(check_launch("cross_entropy_kernel"));
+  }
   mean_kernel<<<1, 1024, 0, s>>>(rows, (int)b, loss);
   return check_launch("mean_kernel");
 }

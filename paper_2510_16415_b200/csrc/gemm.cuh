@@ -81,7 +81,9 @@ __device__ __forceinline__ void store16(void* base, int64_t idx, const float* v,
       reinterpret_cast<uint4*>(p)[0] = w[0];
       reinterpret_cast<uint4*>(p)[1] = w[1];
     } else {
-      for (int j = 0; j < cnt; ++j) p[j] = f2bf(v[j]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cnt) p[j] = f2bf(v[j]);
     }
   } else {
     float* p = reinterpret_cast<float*>(base) + idx;
@@ -90,7 +92,9 @@ __device__ __forceinline__ void store16(void* base, int64_t idx, const float* v,
       for (int j = 0; j < 4; ++j)
         reinterpret_cast<float4*>(p)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     } else {
-      for (int j = 0; j < cnt; ++j) p[j] = v[j];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cnt) p[j] = v[j];
     }
   }
 }
@@ -110,7 +114,8 @@ __device__ __forceinline__ void load16(const void* base, int64_t idx, float* v, 
         v[2 * j + 1] = f.y;
       }
     } else {
-      for (int j = 0; j < cnt; ++j) v[j] = bf2f(p[j]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = j < cnt ? bf2f(p[j]) : 0.f;
     }
   } else {
     const float* p = reinterpret_cast<const float*>(base) + idx;
@@ -121,7 +126,8 @@ __device__ __forceinline__ void load16(const void* base, int64_t idx, float* v, 
         v[4 * j] = f.x; v[4 * j + 1] = f.y; v[4 * j + 2] = f.z; v[4 * j + 3] = f.w;
       }
     } else {
-      for (int j = 0; j < cnt; ++j) v[j] = p[j];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = j < cnt ? p[j] : 0.f;
     }
   }
 }
@@ -165,7 +171,9 @@ __device__ __forceinline__ void epi_apply(const Epilogue& e, int r, int n0, int 
     store16(e.out, idx, v, cnt, e.out_prec);
   } else if (e.kind == EPI_ATOMIC) {
     float* p = reinterpret_cast<float*>(e.out) + (int64_t)r * e.ldo + n0;
-    for (int j = 0; j < cnt; ++j) red_add_f32(p + j, e.alpha * v[j]);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < cnt) red_add_f32(p + j, e.alpha * v[j]);
   } else if (e.kind == EPI_SWIGLU_BWD_CACHED) {
     // acc = d_act; aux holds gate (col n) and up (col offaux + n).
     float g[16], u[16], dg[16], du[16];
@@ -293,9 +301,15 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
+// ---------------------------------------------------------------------------
+// tcgen05 kernel
+// ---------------------------------------------------------------------------
+
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;
-constexpr int TC_THREADS = 256;
+constexpr int TC_EPI_WARPS = 8;                        // 2 per TMEM lane quadrant
+constexpr int TC_THREADS = 128 + 32 * TC_EPI_WARPS;    // warps 0-3: TMA, MMA, TMEM alloc, spare
+constexpr int TC_STAGE_OUT = 4096;                     // per-epilogue-warp staging: 32 rows x 128 B
 
 template <int BN>
 struct TcCfg {
@@ -304,18 +318,166 @@ struct TcCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = TC_EPI_WARPS * TC_STAGE_OUT;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
+
+// Output slot s of an epilogue: 0 = `out`, 1 = `out2`, 2 = `out2 + off2`.
+struct TcOut {
+  int used[3];
+  int prec[3];
+  int reduce[3];  // 1: TMA reduce-add (accumulate / split-K), 0: TMA store
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1, int reduce) {
+  if (reduce)
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  tmem_ld16(taddr, v);
+  tmem_ld16(taddr + 16, v + 16);
+}
+
+// One warp writes its 32 rows x 32 columns to the staging buffer in the TMA
+// swizzle layout (fp32: 128-B rows, SWIZZLE_128B; bf16: 64-B rows,
+// SWIZZLE_64B) and lane 0 issues the bulk store / reduce-add.
+__device__ __forceinline__ void stage_and_store(uint8_t* stg, const CUtensorMap* map, const float* v, int prec,
+                                                int reduce, int c0, int r0, int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+  if (prec == PREC_F32) {
+    uint8_t* row = stg + lane * 128;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      *reinterpret_cast<float4*>(row + ((u ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+  } else {
+    uint8_t* row = stg + lane * 64;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * u + 2 * j], v[8 * u + 2 * j + 1]);
+        w[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      *reinterpret_cast<uint4*>(row + ((u ^ ((lane >> 1) & 3)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) tma_store_2d(map, stg, c0, r0, reduce);
+}
+
+// Epilogue math for output slot `slot` on 32 consecutive output columns n0..
+// of row r (tcgen05 path): 0 = out / act, 1 = gate or d_gate, 2 = up or d_up.
+__device__ __forceinline__ void load32(const void* base, int64_t idx, float* v, int cnt, int prec) {
+  load16(base, idx, v, min(cnt, 16), prec);
+  if (cnt > 16) load16(base, idx + 16, v + 16, cnt - 16, prec);
+}
+
+__device__ __forceinline__ void epi_slot32(const Epilogue& e, int slot, int r, int n0, int cnt, bool row_ok,
+                                           const float* g, const float* u, float* o) {
+  if (e.kind == EPI_STORE || e.kind == EPI_ATOMIC) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = g[j] * e.alpha;
+    if (e.rope_cos && n0 < e.rope_cols && row_ok) {
+      const int pos = r % e.rope_T, half = e.rope_hd >> 1;
+      if ((e.rope_hd & 31) == 0 && n0 + 32 <= e.rope_cols) {
+        // the 32-column chunk lies inside one head: 16 consecutive (cos, sin)
+        const int base = pos * half + ((n0 % e.rope_hd) >> 1);
+        float cs[16], sn[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 c4 = __ldg(reinterpret_cast<const float4*>(e.rope_cos + base) + q);
+          const float4 s4 = __ldg(reinterpret_cast<const float4*>(e.rope_sin + base) + q);
+          cs[4 * q] = c4.x; cs[4 * q + 1] = c4.y; cs[4 * q + 2] = c4.z; cs[4 * q + 3] = c4.w;
+          sn[4 * q] = s4.x; sn[4 * q + 1] = s4.y; sn[4 * q + 2] = s4.z; sn[4 * q + 3] = s4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float ev = o[2 * j], od = o[2 * j + 1];
+          o[2 * j] = ev * cs[j] - od * sn[j];
+          o[2 * j + 1] = ev * sn[j] + od * cs[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int c = n0 + 2 * j;
+          if (c < e.rope_cols) {
+            const int pi = pos * half + ((c % e.rope_hd) >> 1);
+            const float cs = __ldg(e.rope_cos + pi), sn = __ldg(e.rope_sin + pi);
+            const float ev = o[2 * j], od = o[2 * j + 1];
+            o[2 * j] = ev * cs - od * sn;
+            o[2 * j + 1] = ev * sn + od * cs;
+          }
+        }
+      }
+    }
+    if (e.residual && row_ok) {
+      float t[32];
+      load32(e.residual, (int64_t)r * e.ldr + n0, t, cnt, PREC_F32);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) o[j] += t[j];
+    }
+    return;
+  }
+  if (e.kind == EPI_SWIGLU_BWD_CACHED) {  // g = d_act; aux = cached gate | up
+    float gt[32], up[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) { gt[j] = 0.f; up[j] = 0.f; }
+    if (row_ok) {
+      load32(e.aux, (int64_t)r * e.ldaux + n0, gt, cnt, e.act_prec);
+      if (slot == 1) load32(e.aux, (int64_t)r * e.ldaux + e.offaux + n0, up, cnt, e.act_prec);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      o[j] = slot == 2 ? g[j] * silu_f(gt[j])                    // d_up   (model.py:252)
+                       : (g[j] * up[j]) * silu_grad_f(gt[j]);    // d_gate (model.py:251,253)
+    return;
+  }
+  // paired SwiGLU kinds: g = gate, u = up
+  if (slot == 0) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = silu_f(g[j]) * u[j];  // act (model.py:216)
+    return;
+  }
+  if (e.kind == EPI_SWIGLU_FWD) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = slot == 1 ? g[j] : u[j];
+    return;
+  }
+  float d[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) d[j] = 0.f;
+  if (row_ok) load32(e.aux, (int64_t)r * e.ldaux + n0, d, cnt, e.act_prec);
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    o[j] = slot == 2 ? d[j] * silu_f(g[j]) : (d[j] * u[j]) * silu_grad_f(g[j]);
+}
 
 template <int BN, bool A_KMAJOR, bool B_KMAJOR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmDev p) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
+                   const __grid_constant__ CUtensorMap tmO2, GemmDev p, TcOut outs) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sE = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -331,7 +493,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], 32 * TC_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -430,40 +592,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===== Epilogue warps: TMEM -> registers -> fused epilogue -> global =====
+    // ===== Epilogue warps: TMEM -> registers -> fused math -> smem -> TMA =====
     const int ew = warp - 4;
-    const int row_in_tile = ew * 32 + lane;
+    const int quad = ew & 3;        // TMEM lane quadrant == warp % 4
+    const int half = ew >> 2;       // which half of the column chunks
+    uint8_t* stg = sE + ew * TC_STAGE_OUT;
     int acc = 0;
     uint32_t acc_phase = 0;
+    constexpr int NCHUNK_PLAIN = BN / 32;
+    constexpr int NCHUNK_PAIR = BN / 64;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int mt, nt, ks;
       decode_tile(p, t, mt, nt, ks);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mt * TC_BM + row_in_tile;
-      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-      if (!p.paired) {
+      const int r0 = mt * TC_BM + quad * 32;
+      const int row = r0 + lane;
+      const bool row_ok = row < p.M;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
 #pragma unroll 1
-        for (int c = 0; c < BN / 16; ++c) {
-          float v[16];
-          tmem_ld16(taddr + c * 16, v);
-          const int n0 = nt * BN + c * 16;
-          if (row < p.M && n0 < p.N) epi_apply(p.epi, row, n0, min(16, p.N - n0), v);
+      for (int c = half; c < nchunks; c += 2) {
+        float g[32], u[32];
+        int n0;
+        if (!p.paired) {
+          tmem_ld32(taddr + c * 32, g);
+          n0 = nt * BN + c * 32;
+        } else {
+          tmem_ld32(taddr + c * 32, g);
+          tmem_ld32(taddr + BN / 2 + c * 32, u);
+          n0 = nt * (BN / 2) + c * 32;
         }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float g[16], u[16];
-          tmem_ld16(taddr + c * 16, g);
-          tmem_ld16(taddr + BN / 2 + c * 16, u);
-          const int n0 = nt * (BN / 2) + c * 16;
-          if (row < p.M && n0 < p.N) epi_apply_pair(p.epi, row, n0, min(16, p.N - n0), g, u);
+        if (n0 >= p.N) continue;  // warp-uniform
+        const int cnt = min(32, p.N - n0);
+        if (outs.used[0]) {
+          float o[32];
+          epi_slot32(p.epi, 0, row, n0, cnt, row_ok, g, u, o);
+          stage_and_store(stg, &tmO0, o, outs.prec[0], outs.reduce[0], n0, r0, lane);
+        }
+        if (outs.used[1]) {
+          float o[32];
+          epi_slot32(p.epi, 1, row, n0, cnt, row_ok, g, u, o);
+          stage_and_store(stg, &tmO1, o, outs.prec[1], outs.reduce[1], n0, r0, lane);
+        }
+        if (outs.used[2]) {
+          float o[32];
+          epi_slot32(p.epi, 2, row, n0, cnt, row_ok, g, u, o);
+          stage_and_store(stg, &tmO2, o, outs.prec[2], outs.reduce[2], n0, r0, lane);
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();

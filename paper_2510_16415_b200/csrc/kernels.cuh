@@ -232,3 +232,205 @@ __global__ void adamw_kernel(const AdamSeg* __restrict__ segs, int nseg, float* 
 }
 
 }  // namespace mecefo
+
+namespace mecefo {
+
+// ---------------------------------------------------------------------------
+// Bandwidth-oriented versions (the row lives in registers; 16-byte accesses,
+// one warp per row, lane-contiguous float4 columns).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void store4(void* base, int64_t idx, float4 v, int prec) {
+  if (prec == PREC_BF16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&a);
+    w.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + idx) = w;
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + idx) = v;
+  }
+}
+
+// model.py:183-186. Requires m % 4 == 0 and m <= 128 * NV.
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_fwd_vec_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                                              void* __restrict__ out, float* __restrict__ inv_out,
+                                                              int rows, int m, int out_prec) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* xr = x + (int64_t)row * m;
+  float4 v[NV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 4;
+    v[i] = c < m ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  ss = warp_sum(ss);
+  const float inv = 1.f / sqrtf(ss / (float)m + kRmsEps);
+  if (lane == 0 && inv_out) inv_out[row] = inv;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 4;
+    if (c < m) {
+      const float4 s = __ldg(reinterpret_cast<const float4*>(g + c));
+      store4(out, (int64_t)row * m + c,
+             make_float4((v[i].x * inv) * s.x, (v[i].y * inv) * s.y, (v[i].z * inv) * s.z, (v[i].w * inv) * s.w),
+             out_prec);
+    }
+  }
+}
+
+// model.py:189-195 + approx.py:130, fused: dx = resid + a*inv - x*inv^3*(sum(a*x)/m),
+// a = d*g; dx_lp = compute-precision copy; per-block partial column sums of
+// d*x*inv (scale gradient), reduced in a fixed order afterwards.
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_vec_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                                              const float* __restrict__ inv,
+                                                              const float* __restrict__ d,
+                                                              const float* __restrict__ resid, float* __restrict__ dx,
+                                                              void* __restrict__ dx_lp, int lp_prec,
+                                                              float* __restrict__ partial, int rows, int m,
+                                                              int rows_per_block) {
+  extern __shared__ float4 red_dyn[];  // [8][NV * 32]
+  float4 (*red)[NV * 32] = reinterpret_cast<float4 (*)[NV * 32]>(red_dyn);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4 gs[NV], acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 4;
+    gs[i] = c < m ? __ldg(reinterpret_cast<const float4*>(g + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(r0 + rows_per_block, rows);
+  for (int row = r0 + wid; row < r1; row += 8) {
+    const float* xr = x + (int64_t)row * m;
+    const float* dr = d + (int64_t)row * m;
+    const float iv = inv[row];
+    float4 xv[NV], dv[NV];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 4;
+      if (c < m) {
+        xv[i] = *reinterpret_cast<const float4*>(xr + c);
+        dv[i] = *reinterpret_cast<const float4*>(dr + c);
+      } else {
+        xv[i] = dv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      s += dv[i].x * gs[i].x * xv[i].x + dv[i].y * gs[i].y * xv[i].y + dv[i].z * gs[i].z * xv[i].z +
+           dv[i].w * gs[i].w * xv[i].w;
+      acc[i].x += dv[i].x * xv[i].x * iv;
+      acc[i].y += dv[i].y * xv[i].y * iv;
+      acc[i].z += dv[i].z * xv[i].z * iv;
+      acc[i].w += dv[i].w * xv[i].w * iv;
+    }
+    s = warp_sum(s) / (float)m;
+    const float k = iv * iv * iv * s;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 4;
+      if (c < m) {
+        float4 o = make_float4(dv[i].x * gs[i].x * iv - xv[i].x * k, dv[i].y * gs[i].y * iv - xv[i].y * k,
+                               dv[i].z * gs[i].z * iv - xv[i].z * k, dv[i].w * gs[i].w * iv - xv[i].w * k);
+        if (resid) {
+          const float4 rr = *reinterpret_cast<const float4*>(resid + (int64_t)row * m + c);
+          o.x += rr.x; o.y += rr.y; o.z += rr.z; o.w += rr.w;
+        }
+        *reinterpret_cast<float4*>(dx + (int64_t)row * m + c) = o;
+        if (dx_lp) store4(dx_lp, (int64_t)row * m + c, o, lp_prec);
+      }
+    }
+  }
+  if (!partial) return;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) red[wid][i * 32 + lane] = acc[i];
+  __syncthreads();
+  for (int q = threadIdx.x; q < NV * 32; q += blockDim.x) {
+    const int c = q * 4;
+    if (c >= m) continue;
+    float4 t = red[0][q];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      t.x += red[w][q].x; t.y += red[w][q].y; t.z += red[w][q].z; t.w += red[w][q].w;
+    }
+    *reinterpret_cast<float4*>(partial + (int64_t)blockIdx.x * m + c) = t;
+  }
+}
+
+// Single-read fused softmax-CE for bf16 logits (model.py:492-509): the row is
+// held in registers (8 bf16 per 16-byte vector, NV vectors per thread), so the
+// logits are read once and dlogits written once.
+template <int NV>
+__global__ void __launch_bounds__(512) cross_entropy_bf16_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
+                                                                  const int64_t* __restrict__ targets,
+                                                                  float* __restrict__ loss_rows, int rows, int V,
+                                                                  float inv_n, int* __restrict__ bad_target) {
+  __shared__ float red[32];
+  __shared__ float zt_s;
+  const int row = blockIdx.x;
+  __nv_bfloat16* lr = logits + (int64_t)row * ld;
+  const int64_t t = targets[row];
+  if (t < 0 || t >= V) {
+    if (threadIdx.x == 0) atomicExch(bad_target, 1);
+    return;
+  }
+  if (threadIdx.x == 0) zt_s = __bfloat162float(lr[t]);
+  uint4 w[NV];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 8;
+    if (c < V) {
+      w[i] = *reinterpret_cast<const uint4*>(lr + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        mx = fmaxf(mx, fmaxf(f.x, f.y));
+      }
+    }
+  }
+  mx = block_max(mx, red);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 8;
+    if (c < V) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        s += __expf(f.x - mx) + __expf(f.y - mx);
+      }
+    }
+  }
+  s = block_sum(s, red);
+  const float lse = mx + logf(s);
+  if (threadIdx.x == 0) loss_rows[row] = lse - zt_s;
+  const float sc = inv_n / s;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 8;
+    if (c < V) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        float p0 = __expf(f.x - mx) * sc, p1 = __expf(f.y - mx) * sc;
+        if (c + 2 * j == t) p0 -= inv_n;
+        if (c + 2 * j + 1 == t) p1 -= inv_n;
+        __nv_bfloat162 q = __floats2bfloat162_rn(p0, p1);
+        o[j] = *reinterpret_cast<uint32_t*>(&q);
+      }
+      *reinterpret_cast<uint4*>(lr + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+}  // namespace mecefo
