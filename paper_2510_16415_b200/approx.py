@@ -79,29 +79,37 @@ class ProjectionCache:
         """Inject a basis (e.g. the reference's seeded V1 for parity)."""
         t = torch.as_tensor(v1).to("cuda", torch.float32).contiguous()
         self.basis[kind] = t
-        self._packed.pop(kind, None)
+        self._packed.clear()
 
     def packed(self, precision: str):
         """Projection struct + keep-alive tensors for the engine."""
-        dt = runtime.compute_dtype(precision)
         ranks = [int(self.basis[k].shape[1]) for k in FFN_KINDS]
         rp = _pad16(max(ranks))
-        keep = []
-        v1p, v1tp = [], []
-        for k in FFN_KINDS:
-            key = (k, precision, rp)
-            if key not in self._packed:
+        key = (precision, rp)
+        if key not in self._packed:
+            dt = runtime.compute_dtype(precision)
+            dev = self.basis["gate"].device
+            n_gu = self.basis["gate"].shape[0]
+            # gate/up transposed bases stacked: one GEMM forms [P_gate | P_up]
+            vt_gu = torch.zeros(2 * rp, n_gu, dtype=dt, device=dev)
+            tensors = {}
+            for i, k in enumerate(FFN_KINDS):
                 b = self.basis[k]
                 n_in, r = b.shape
-                v = torch.zeros(n_in, rp, dtype=dt, device=b.device)
+                v = torch.zeros(n_in, rp, dtype=dt, device=dev)
                 v[:, :r] = b.to(dt)
-                self._packed[key] = (v, v.t().contiguous())
-            v, vt = self._packed[key]
-            keep += [v, vt]
-            v1p.append(v.data_ptr())
-            v1tp.append(vt.data_ptr())
-        st = _lib.Projection((ctypes.c_int32 * 3)(*ranks), rp, (ctypes.c_void_p * 3)(*v1p),
-                             (ctypes.c_void_p * 3)(*v1tp))
+                if k in ("gate", "up") and n_in == n_gu:
+                    vt = vt_gu[i * rp:(i + 1) * rp]
+                    vt.copy_(v.t())
+                else:
+                    vt = v.t().contiguous()
+                tensors[k] = (v, vt)
+            keep = [vt_gu] + [t for k in FFN_KINDS for t in tensors[k]]
+            st = _lib.Projection((ctypes.c_int32 * 3)(*ranks), rp,
+                                 (ctypes.c_void_p * 3)(*[tensors[k][0].data_ptr() for k in FFN_KINDS]),
+                                 (ctypes.c_void_p * 3)(*[tensors[k][1].data_ptr() for k in FFN_KINDS]))
+            self._packed[key] = (st, keep)
+        st, keep = self._packed[key]
         return st, keep, rp
 
 

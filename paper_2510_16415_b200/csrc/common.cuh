@@ -75,9 +75,10 @@ __device__ __forceinline__ float block_max(float v, float* red) {
 
 // SiLU and its derivative, same formulas as the reference
 // (pkg/src/faultsim/model.py:198-204), evaluated in fp32.
-__device__ __forceinline__ float silu_f(float z) { return z / (1.f + expf(-z)); }
+__device__ __forceinline__ float sigmoid_f(float z) { return __frcp_rn(1.f + __expf(-z)); }
+__device__ __forceinline__ float silu_f(float z) { return z * sigmoid_f(z); }
 __device__ __forceinline__ float silu_grad_f(float z) {
-  const float s = 1.f / (1.f + expf(-z));
+  const float s = sigmoid_f(z);
   return s * (1.f + z * (1.f - s));
 }
 

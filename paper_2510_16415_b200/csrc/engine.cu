@@ -16,6 +16,7 @@
 #include "../../include/mecefo.h"
 #include "attention.cuh"
 #include "attention_tc.cuh"
+#include "gemm_dual.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -298,10 +299,30 @@ int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   return launch_tc<BN, false, false>(e, g, s);
 }
 
+// Tile width for the tcgen05 path. The MMA time of a tile is proportional to
+// BN, so the kernel time is ~ waves(BN) * BN with waves = ceil(tiles / 148);
+// pick the BN minimising it, and on ties the widest (better L2 arithmetic
+// intensity: 128x256 tiles read 85 flop/B, 128x64 only 51).
+int choose_bn(const GemmCall& g) {
+  const int64_t nacc = g.paired ? 2 * g.N : g.N;
+  const int64_t tm = (g.M + 127) / 128;
+  // per-flop penalty of narrower tiles (L2-bound operand traffic), measured
+  int best = 64;
+  double best_cost = 1e30;
+  for (int BN : {256, 128, 64}) {
+    if (BN > 64 && nacc <= BN / 2) continue;
+    const int64_t cpt = g.paired ? BN / 2 : BN;
+    const int64_t tiles = tm * ((g.N + cpt - 1) / cpt);
+    const double eff = BN == 256 ? 1.0 : (BN == 128 ? 1.15 : 1.35);
+    const double cost = (double)((tiles + kNumSMs - 1) / kNumSMs) * BN * eff;
+    if (cost < best_cost * 0.999) { best_cost = cost; best = BN; }
+  }
+  return best;
+}
+
 int tiles_for(const GemmCall& g, int prec) {
   if (prec == PREC_BF16) {
-    const int64_t nacc = g.paired ? 2 * g.N : g.N;
-    const int BN = nacc >= 256 ? 256 : (nacc > 64 ? 128 : 64);
+    const int BN = choose_bn(g);
     const int64_t cpt = g.paired ? BN / 2 : BN;
     return (int)(((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt));
   }
@@ -320,9 +341,9 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     return set_err(MECEFO_ERR_CONSISTENCY, "split-K requires the atomic epilogue");
   if (e->prec == PREC_BF16) {
     if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
-    const int64_t nacc = g.paired ? 2 * g.N : g.N;
-    if (nacc >= 256) return dispatch_tc_major<256>(e, g, s);
-    if (nacc > 64) return dispatch_tc_major<128>(e, g, s);
+    const int BN = choose_bn(g);
+    if (BN == 256) return dispatch_tc_major<256>(e, g, s);
+    if (BN == 128) return dispatch_tc_major<128>(e, g, s);
     return dispatch_tc_major<64>(e, g, s);
   }
   GemmDev p{};
@@ -440,6 +461,38 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
     TRY(check_launch("colsum_finalize_kernel"));
   }
   return MECEFO_OK;
+}
+
+// Fused d_act / gate / up tcgen05 kernel + SwiGLU backward epilogue (bf16).
+int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const void* w_down_c, const void* w_gu_c,
+                    void* act, void* dcat, int64_t b, cudaStream_t s) {
+  const int64_t m = e->d.hidden, f = e->d.ffn;
+  ProfScope prof("nbr.fused_recompute_swiglu_bwd", 2.0 * b * f * m * 3.0,
+                 2.0 * (2.0 * b * m + 3.0 * f * m) + 2.0 * b * f * (act ? 3 : 2), s);
+  CUtensorMap tdy, th2, twd, twgu, tact, tdg, tdu;
+  TRY(make_tmap(e, &tdy, dy_c, m, b, m, 64, TC_BM));
+  TRY(make_tmap(e, &th2, h2, m, b, m, 64, TC_BM));
+  TRY(make_tmap(e, &twd, w_down_c, f, m, f, 64, 64));
+  TRY(make_tmap(e, &twgu, w_gu_c, m, 2 * f, m, 64, 64));
+  std::memset(&tact, 0, sizeof(tact));
+  if (act) TRY(make_tmap(e, &tact, act, f, b, f, 32, 32, 0, 64));
+  TRY(make_tmap(e, &tdg, dcat, f, b, 2 * f, 32, 32, 0, 64));
+  TRY(make_tmap(e, &tdu, reinterpret_cast<uint8_t*>(dcat) + f * 2, f, b, 2 * f, 32, 32, 0, 64));
+  DualDev p{};
+  p.M = (int)b; p.NP = (int)f; p.K = (int)m; p.f_off = f;
+  p.kblocks = (int)((m + TC_BK - 1) / TC_BK);
+  p.tiles_m = (int)((b + TC_BM - 1) / TC_BM);
+  p.tiles_n = (int)((f + DU_NP - 1) / DU_NP);
+  p.num_tiles = p.tiles_m * p.tiles_n;
+  p.has_act = act ? 1 : 0;
+  static bool set = false;
+  if (!set) {
+    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
+    set = true;
+  }
+  swiglu_bwd_dual_kernel<<<std::min(p.num_tiles, kNumSMs), TC_THREADS, DU_SMEM, s>>>(tdy, th2, twd, twgu, tact, tdg,
+                                                                                     tdu, p);
+  return check_launch("swiglu_bwd_dual_kernel");
 }
 
 int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cudaStream_t s) {
@@ -700,26 +753,48 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
   void* P;
   float* Q;
   void* Qc;
-  TRY(ws.take(b * rp * ps, &P));
+  TRY(ws.take(b * 2 * rp * ps, &P));
   TRY(ws.take(std::max(m, f) * rp * 4, reinterpret_cast<void**>(&Q)));
   if (e->prec == PREC_BF16) TRY(ws.take(std::max(m, f) * rp * ps, &Qc));
   else Qc = Q;
+  for (int k = 0; k < 3; ++k)
+    if (kinds[k].grad && (!pj->v1[k] || !pj->v1t[k]))
+      return set_err(MECEFO_ERR_CONTRACT, "projection basis %d missing", k);
+  // gate and up share inp2 = h2: when their V1^T are stacked contiguously,
+  // one GEMM produces [P_gate | P_up] (b, 2 rp).
+  const bool merged = kinds[0].grad && kinds[1].grad &&
+                      reinterpret_cast<const uint8_t*>(pj->v1t[1]) ==
+                          reinterpret_cast<const uint8_t*>(pj->v1t[0]) + rp * m * ps;
+  if (merged) {
+    GemmCall g;
+    g.M = b; g.N = 2 * rp; g.K = m;
+    g.a = {h2, m, true}; g.b = {pj->v1t[0], m, true};
+    g.epi = epi_store(P, 2 * rp, e->prec);
+    g.tag = "lowrank.P";
+    TRY(run_gemm(e, g, s));
+  }
   for (int k = 0; k < 3; ++k) {
     const K& kd = kinds[k];
     if (!kd.grad) continue;
-    if (!pj->v1[k] || !pj->v1t[k]) return set_err(MECEFO_ERR_CONTRACT, "projection basis %d missing", k);
-    // P = inp2 V1  (b, rp)
-    GemmCall g;
-    g.M = b; g.N = rp; g.K = kd.n_in;
-    g.a = {kd.inp, kd.n_in, true}; g.b = {pj->v1t[k], kd.n_in, true};
-    g.epi = epi_store(P, rp, e->prec);
-    g.tag = "lowrank.P";
-    TRY(run_gemm(e, g, s));
+    const void* Pk = P;
+    int64_t ldp = rp;
+    if (merged && k < 2) {
+      Pk = reinterpret_cast<const uint8_t*>(P) + k * rp * ps;
+      ldp = 2 * rp;
+    } else {
+      // P = inp2 V1  (b, rp)
+      GemmCall g;
+      g.M = b; g.N = rp; g.K = kd.n_in;
+      g.a = {kd.inp, kd.n_in, true}; g.b = {pj->v1t[k], kd.n_in, true};
+      g.epi = epi_store(P, rp, e->prec);
+      g.tag = "lowrank.P";
+      TRY(run_gemm(e, g, s));
+    }
     // Q = d2^T P  (n_out, rp), K = b: the long-K "small contraction"
     CUDA_TRY(cudaMemsetAsync(Q, 0, kd.n_out * rp * 4, s));
-    g = GemmCall();
+    GemmCall g;
     g.M = kd.n_out; g.N = rp; g.K = b;
-    g.a = {kd.d2, kd.ldd, false}; g.b = {P, rp, false};
+    g.a = {kd.d2, kd.ldd, false}; g.b = {Pk, ldp, false};
     g.tag = "lowrank.Q";
     TRY(gemm_accumulate(e, g, Q, rp, 1.f, s));
     if (e->prec == PREC_BF16) TRY(cast_to_compute(e, Q, Qc, kd.n_out * rp, s));
@@ -765,25 +840,31 @@ int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights*
   TRY(ws.take(b * m * 4, reinterpret_cast<void**>(&dh)));
   // recompute h2 = rmsnorm(x1) (approx.py:128 -> model.py:213)
   TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
-  // d_act = dy Wd  (model.py:248); Wd is (m, f) = B MN-major
   GemmCall g;
-  g.M = b; g.N = f; g.K = m;
-  g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
-  g.epi = epi_store(d_act, f, e->prec);
-  g.tag = "nbr.d_act";
-  TRY(run_gemm(e, g, s));
-  // recompute gate/up on the tensor cores; the epilogue forms act and the
-  // SwiGLU backward (model.py:214-216, 250-253): gate/up never touch HBM.
-  g = GemmCall();
-  g.M = b; g.N = f; g.K = m;
-  g.a = {h2, m, true}; g.b = {lw->w_gu_c, m, true};
-  g.paired = true; g.pair_off = f;
-  Epilogue ep{};
-  ep.kind = EPI_SWIGLU_BWD_RECOMP; ep.out = act; ep.ldo = f; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
-  ep.aux = d_act; ep.ldaux = f; ep.act_prec = e->prec;
-  g.epi = ep;
-  g.tag = "nbr.gu_recompute_swiglu_bwd";
-  TRY(run_gemm(e, g, s));
+  if (e->prec == PREC_BF16) {
+    // d_act = dy Wd, gate|up recomputed = h2 [Wg;Wu]^T, both into TMEM of one
+    // kernel; its epilogue forms act and the SwiGLU backward (model.py:214-216,
+    // 248-253): gate, up and d_act never touch HBM.
+    TRY(swiglu_bwd_dual(e, dy_c, h2, lw->w_down_c, lw->w_gu_c, act, dcat, b, s));
+  } else {
+    // fp32 mode: d_act = dy Wd (model.py:248; Wd is (m, f) = B MN-major), then the
+    // recompute GEMM whose epilogue reads d_act.
+    g.M = b; g.N = f; g.K = m;
+    g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
+    g.epi = epi_store(d_act, f, e->prec);
+    g.tag = "nbr.d_act";
+    TRY(run_gemm(e, g, s));
+    g = GemmCall();
+    g.M = b; g.N = f; g.K = m;
+    g.a = {h2, m, true}; g.b = {lw->w_gu_c, m, true};
+    g.paired = true; g.pair_off = f;
+    Epilogue ep{};
+    ep.kind = EPI_SWIGLU_BWD_RECOMP; ep.out = act; ep.ldo = f; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
+    ep.aux = d_act; ep.ldaux = f; ep.act_prec = e->prec;
+    g.epi = ep;
+    g.tag = "nbr.gu_recompute_swiglu_bwd";
+    TRY(run_gemm(e, g, s));
+  }
   // d_h2 = [d_gate | d_up] [Wg; Wu]  (model.py:258), K = 2f
   g = GemmCall();
   g.M = b; g.N = m; g.K = 2 * f;
@@ -847,14 +928,18 @@ int mecefo_backward_block_exact(mecefo_engine* e, const mecefo_layer_weights* lw
   TRY(ws.take(b * H * 4, reinterpret_cast<void**>(&dsum)));
   // ---- FFN sub-block (model.py:232-261) ----
   GemmCall g;
-  g.M = b; g.N = f; g.K = m;
-  g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
-  Epilogue ep{};
-  ep.kind = EPI_SWIGLU_BWD_CACHED; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
-  ep.aux = c->gu; ep.ldaux = 2 * f; ep.offaux = f; ep.act_prec = e->prec;
-  g.epi = ep;
-  g.tag = "exact.d_act_swiglu_bwd";
-  TRY(run_gemm(e, g, s));
+  if (e->prec == PREC_BF16) {
+    TRY(swiglu_bwd_dual(e, dy_c, c->h2, lw->w_down_c, lw->w_gu_c, nullptr, dcat, b, s));
+  } else {
+    g.M = b; g.N = f; g.K = m;
+    g.a = {dy_c, m, true}; g.b = {lw->w_down_c, f, false};
+    Epilogue ep{};
+    ep.kind = EPI_SWIGLU_BWD_CACHED; ep.out2 = dcat; ep.ldo2 = 2 * f; ep.off2 = f;
+    ep.aux = c->gu; ep.ldaux = 2 * f; ep.offaux = f; ep.act_prec = e->prec;
+    g.epi = ep;
+    g.tag = "exact.d_act_swiglu_bwd";
+    TRY(run_gemm(e, g, s));
+  }
   g = GemmCall();
   g.M = b; g.N = m; g.K = 2 * f;
   g.a = {dcat, 2 * f, true}; g.b = {lw->w_gu_c, m, false};
@@ -1019,14 +1104,11 @@ int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets,
   TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
   ProfScope prof("cross_entropy", 0.0, 2.0 * b * V * e->ps, s);
-  const int nv = (int)((V + 512 * 8 - 1) / (512 * 8));
-  auto* lg = reinterpret_cast<__nv_bfloat16*>(logits);
-  if (e->prec == PREC_BF16 && V % 8 == 0 && nv <= 16) {
-    if (nv <= 2) cross_entropy_bf16_kernel<2><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
-    else if (nv <= 4) cross_entropy_bf16_kernel<4><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
-    else if (nv <= 8) cross_entropy_bf16_kernel<8><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
-    else cross_entropy_bf16_kernel<16><<<(unsigned)b, 512, 0, s>>>(lg, V, targets, rows, (int)b, (int)V, 1.f / (float)b, bad);
-    TRY(check_launch("cross_entropy_bf16_kernel"));
+  if (e->prec == PREC_BF16 && V % 8 == 0) {
+    cross_entropy_warp_kernel<<<(unsigned)((b + 7) / 8), 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(logits), V,
+                                                                       targets, rows, (int)b, (int)V, 1.f / (float)b,
+                                                                       bad);
+    TRY(check_launch("cross_entropy_warp_kernel"));
   } else {
     cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
                                                       bad);

@@ -1,0 +1,172 @@
+// Fused FFN recompute + SwiGLU backward on the tensor cores (the MeCeFO
+// neighbour-backward hot kernel; approx.py:128-129 -> model.py:214-216,
+// 248-253).
+//
+// For a tile of 128 tokens x 64 FFN columns, ONE kernel accumulates three
+// tcgen05 products over the hidden dimension into TMEM:
+//     d_act = dy  W_down          (B = W_down read MN-major, no transpose)
+//     gate  = h2  W_gate^T        (recomputed)
+//     up    = h2  W_up^T          (recomputed)
+// and the epilogue emits act = silu(gate)*up, d_gate = d_act*up*silu'(gate)
+// and d_up = d_act*silu(gate) through swizzled smem + TMA stores. gate, up and
+// d_act never touch HBM, and no epilogue operand is read from
+// global memory.
+#pragma once
+#include "gemm.cuh"
+
+namespace mecefo {
+
+constexpr int DU_NP = 64;                                   // pair columns per tile
+constexpr int DU_A_BYTES = TC_BM * TC_BK * 2;               // 16 KB (per A operand)
+constexpr int DU_B1_BYTES = DU_NP * TC_BK * 2;              // 8 KB  (W_down, MN-major)
+constexpr int DU_B2_BYTES = 2 * DU_NP * TC_BK * 2;          // 16 KB (gate | up rows)
+constexpr int DU_STAGE_BYTES = 2 * DU_A_BYTES + DU_B1_BYTES + DU_B2_BYTES;  // 56 KB
+constexpr int DU_STAGES = 3;
+constexpr int DU_SMEM = DU_STAGES * DU_STAGE_BYTES + TC_EPI_WARPS * TC_STAGE_OUT + 1024 + 256;
+
+struct DualDev {
+  int M, NP, K;     // tokens, FFN width f, hidden m
+  int64_t f_off;    // row offset of W_up inside W_gu (= f)
+  int kblocks, tiles_m, tiles_n, num_tiles;
+  int has_act;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    swiglu_bwd_dual_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmH2,
+                           const __grid_constant__ CUtensorMap tmWd, const __grid_constant__ CUtensorMap tmWgu,
+                           const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmDg,
+                           const __grid_constant__ CUtensorMap tmDu, DualDev p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sE = smem + DU_STAGES * DU_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + TC_EPI_WARPS * TC_STAGE_OUT);
+  uint64_t* empty = full + DU_STAGES;
+  uint64_t* tfull = empty + DU_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DU_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 32 * TC_EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int mt = t % p.tiles_m, nt = t / p.tiles_m;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], DU_STAGE_BYTES);
+          uint8_t* st = smem + stage * DU_STAGE_BYTES;
+          const int k0 = kb * TC_BK;
+          tma_load_2d(st, &tmDy, &full[stage], k0, mt * TC_BM);
+          tma_load_2d(st + DU_A_BYTES, &tmH2, &full[stage], k0, mt * TC_BM);
+          tma_load_2d(st + 2 * DU_A_BYTES, &tmWd, &full[stage], nt * DU_NP, k0);
+          uint8_t* b2 = st + 2 * DU_A_BYTES + DU_B1_BYTES;
+          tma_load_2d(b2, &tmWgu, &full[stage], k0, nt * DU_NP);
+          tma_load_2d(b2 + DU_NP * 128, &tmWgu, &full[stage], k0, nt * DU_NP + (int)p.f_off);
+          if (++stage == DU_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer =====
+      // d_act: A K-major, B MN-major, N = 64; gate|up: both K-major, N = 128
+      constexpr uint32_t id1 = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t id2 = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * 256;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + stage * DU_STAGE_BYTES);
+          const uint32_t a1 = st, a2 = st + DU_A_BYTES, b1 = st + 2 * DU_A_BYTES, b2 = b1 + DU_B1_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint32_t acc_on = (kb > 0 || k > 0) ? 1u : 0u;
+            tc_mma_bf16(d0, make_sdesc(a1 + k * 32, 16, 1024), make_sdesc(b1 + k * 2048, 8192, 1024), id1, acc_on);
+            tc_mma_bf16(d0 + 64, make_sdesc(a2 + k * 32, 16, 1024), make_sdesc(b2 + k * 32, 16, 1024), id2, acc_on);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == DU_STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {  // ===== epilogue: 8 warps, one 32-column chunk each =====
+    const int ew = warp - 4, quad = ew & 3, half = ew >> 2;
+    uint8_t* stg = sE + ew * TC_STAGE_OUT;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int mt = t % p.tiles_m, nt = t / p.tiles_m;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int r0 = mt * TC_BM + quad * 32;
+      const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256 + half * 32;
+      float d[32], g[32], u[32];
+      tmem_ld32(ta, d);
+      tmem_ld32(ta + 64, g);
+      tmem_ld32(ta + 128, u);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);  // TMEM drained into registers: release it to the MMA early
+      const int n0 = nt * DU_NP + half * 32;
+      if (n0 < p.NP) {
+        // g <- sigmoid(gate), kept for all three outputs (one exp per element)
+        float sg[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sg[j] = sigmoid_f(g[j]);
+        float o[32];
+        if (p.has_act) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = g[j] * sg[j] * u[j];                              // act
+          stage_and_store(stg, &tmAct, o, PREC_BF16, 0, n0, r0, lane);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = (d[j] * u[j]) * (sg[j] * (1.f + g[j] * (1.f - sg[j])));  // d_gate
+        stage_and_store(stg, &tmDg, o, PREC_BF16, 0, n0, r0, lane);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = d[j] * (g[j] * sg[j]);                              // d_up
+        stage_and_store(stg, &tmDu, o, PREC_BF16, 0, n0, r0, lane);
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
+  }
+}
+
+}  // namespace mecefo

@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_vec_kernel(const float* __res
 // held in registers (8 bf16 per 16-byte vector, NV vectors per thread), so the
 // logits are read once and dlogits written once.
 template <int NV>
-__global__ void __launch_bounds__(512) cross_entropy_bf16_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
+__global__ void __launch_bounds__(256) cross_entropy_bf16_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
                                                                   const int64_t* __restrict__ targets,
                                                                   float* __restrict__ loss_rows, int rows, int V,
                                                                   float inv_n, int* __restrict__ bad_target) {
@@ -430,6 +430,71 @@ __global__ void __launch_bounds__(512) cross_entropy_bf16_kernel(__nv_bfloat16* 
       }
       *reinterpret_cast<uint4*>(lr + c) = make_uint4(o[0], o[1], o[2], o[3]);
     }
+  }
+}
+
+// One warp per row (model.py:492-509, bf16 logits): pass 1 keeps an online
+// (max, sum-exp) per lane over 16-byte vectors, a shuffle reduction merges the
+// lanes; pass 2 re-reads the row (L2-resident: 64 KB per row) and writes
+// dlogits = (softmax - onehot)/n in place. No block barriers, full occupancy.
+__global__ void __launch_bounds__(256) cross_entropy_warp_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
+                                                                  const int64_t* __restrict__ targets,
+                                                                  float* __restrict__ loss_rows, int rows, int V,
+                                                                  float inv_n, int* __restrict__ bad_target) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  __nv_bfloat16* lr = logits + (int64_t)row * ld;
+  const int64_t t = targets[row];
+  if (t < 0 || t >= V) {
+    if (lane == 0) atomicExch(bad_target, 1);
+    return;
+  }
+  const float zt = __bfloat162float(lr[t]);
+  float mx = -INFINITY, s = 0.f;
+  for (int c = lane * 8; c < V; c += 256) {
+    const uint4 w = *reinterpret_cast<const uint4*>(lr + c);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+    float f[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 q = __bfloat1622float2(h[j]);
+      f[2 * j] = q.x;
+      f[2 * j + 1] = q.y;
+    }
+    float lm = f[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) lm = fmaxf(lm, f[j]);
+    const float nm = fmaxf(mx, lm);
+    s = s * __expf(mx - nm);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += __expf(f[j] - nm);
+    mx = nm;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+    const float os = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(mx, om);
+    s = (mx == -INFINITY ? 0.f : s * __expf(mx - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    mx = nm;
+  }
+  if (lane == 0) loss_rows[row] = mx + logf(s) - zt;
+  const float sc = inv_n / s;
+  for (int c = lane * 8; c < V; c += 256) {
+    const uint4 w = *reinterpret_cast<const uint4*>(lr + c);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+    uint32_t o4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 q = __bfloat1622float2(h[j]);
+      float p0 = __expf(q.x - mx) * sc, p1 = __expf(q.y - mx) * sc;
+      if (c + 2 * j == t) p0 -= inv_n;
+      if (c + 2 * j + 1 == t) p1 -= inv_n;
+      __nv_bfloat162 r = __floats2bfloat162_rn(p0, p1);
+      o4[j] = *reinterpret_cast<uint32_t*>(&r);
+    }
+    *reinterpret_cast<uint4*>(lr + c) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
   }
 }
 
