@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fault-free", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--eager", action="store_true", help="launch kernels eagerly instead of CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
 
@@ -240,23 +241,32 @@ def main():
         if group is not None:
             dist.barrier()
 
-    def timed(mbs, skip, steps, e2e=False, profile=False):
+    def timed(mbs, skip, steps, e2e=False, profile=False, graph=False):
+        """K steps bracketed by barrier + synchronize; device time (CUDA events
+        on the launching stream), max over ranks. graph=True replays the
+        captured CUDA graph of the same plan (eager fallback when a projection
+        refresh is due)."""
         barrier()
         torch.cuda.synchronize()
         if profile:
             lib.mecefo_profile_enable(1)
         n0 = lib.mecefo_launch_count()
+        replays = 0
         t_wall = time.perf_counter()
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st.record()
         for _ in range(steps):
-            losses = eng.step(mbs, R, lr, skip=skip, check=False)
+            if graph and not eng.projections_due(mbs):
+                losses = eng.replay(lr)
+                replays += 1
+            else:
+                losses = eng.step(mbs, R, lr, skip=skip, check=False)
             if e2e:
                 losses.cpu()  # D2H read of the step's result
         en.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t_wall
-        launches = lib.mecefo_launch_count() - n0
+        launches = lib.mecefo_launch_count() - n0 + replays * graph_launches.get(id(mbs), 0)
         ms = st.elapsed_time(en)
         barrier()
         if group is not None:
@@ -264,6 +274,15 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, launches, wall
+
+    graph_launches = {}
+
+    def capture(mbs, skip):
+        """Eager step (warms descriptors / caches) then capture the plan."""
+        eng.step(mbs, R, lr, skip=skip, check=False)
+        n0 = lib.mecefo_launch_count()
+        eng.capture(mbs, R, skip)
+        graph_launches[id(mbs)] = (lib.mecefo_launch_count() - n0) // 2
 
     # warm-up (includes the first projection refresh of every lean layer)
     for _ in range(args.warmup):
@@ -278,10 +297,18 @@ def main():
             print(json.dumps({"profile_only": True, "ms_per_step": ms / args.steps}), flush=True)
         return
 
+    # value: CUDA-graph replay of the degraded iteration, inputs resident in HBM
+    use_graph = not args.eager
+    if use_graph:
+        capture(degraded, skip_d)
     with ClockSampler(local) as clk:
-        ms, launches, wall = timed(degraded, skip_d, args.steps, profile=True)
+        ms, launches, wall = timed(degraded, skip_d, args.steps, graph=use_graph)
     tokens_per_step = R * b
     value = tokens_per_step * args.steps / (ms / 1000.0)
+    # per-kernel attribution: the same degraded iteration, eager, with CUDA
+    # events around every kernel group (own timed region of K steps)
+    ms_prof, _, _ = timed(degraded, skip_d, args.steps, profile=True)
+    ms_eager = ms_prof
 
     # dominant kernel roofline from the live profile of the timed region
     n = lib.mecefo_profile_count()
@@ -305,8 +332,9 @@ def main():
     top = sorted(agg.items(), key=lambda kv: -kv[1][0])
     roofline = None
     kernels = []
-    for tag, (tms, cnt, fl, by) in top[:12]:
-        kernels.append({"tag": tag, "ms_total": round(tms, 3), "launches": cnt, "share": round(tms / ms, 4),
+    kernel_ms = sum(v[0] for v in agg.values())
+    for tag, (tms, cnt, fl, by) in top[:16]:
+        kernels.append({"tag": tag, "ms_total": round(tms, 3), "launches": cnt, "share": round(tms / ms_prof, 4),
                         "tflops": round(fl / (tms / 1e3) / 1e12, 1) if fl else None,
                         "gbs": round(by / (tms / 1e3) / 1e9, 1)})
     if top:
@@ -317,26 +345,30 @@ def main():
             roofline = {"kernel": tag, "bound": "tensor", "achieved": round(ach, 1), "peak": bf16_sus,
                         "unit": "TFLOP/s", "frac": round(ach / bf16_sus, 4), "traffic": None,
                         "per_launch": f"{fl / cnt / 1e9:.3f} GFLOP algorithmic (2*M*N*K)",
-                        "peak_source": f"{peak_src} bf16 sustained", "share_of_step": round(tms / ms, 4)}
+                        "peak_source": f"{peak_src} bf16 sustained", "share_of_step": round(tms / ms_prof, 4)}
         else:
             ach = by / cnt / avg_s / 1e9
             roofline = {"kernel": tag, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                         "frac": round(ach / hbm, 4), "traffic": None,
                         "per_launch": f"{by / cnt / 1e6:.2f} MB algorithmic", "peak_source": peak_src,
-                        "share_of_step": round(tms / ms, 4)}
+                        "share_of_step": round(tms / ms_prof, 4)}
 
     # fault-free step (every GPU one exact microbatch) and instantaneous drop
     ff_value = None
     if not args.no_fault_free:
         for _ in range(2):
             eng.step(fault_free, R, lr, skip=skip_f, check=False)
-        ms_ff, _, _ = timed(fault_free, skip_f, args.steps)
+        if use_graph:
+            capture(fault_free, skip_f)
+        ms_ff, _, _ = timed(fault_free, skip_f, args.steps, graph=use_graph)
         ff_value = tokens_per_step * args.steps / (ms_ff / 1000.0)
 
     # end-to-end through the public API: H2D of inputs + D2H of the loss per step
-    for _ in range(1):
+    if use_graph:
+        capture(degraded_e2e, skip_d)
+    else:
         eng.step(degraded_e2e, R, lr, skip=skip_d, check=False)
-    ms_e2e, _, _ = timed(degraded_e2e, skip_d, args.steps, e2e=True)
+    ms_e2e, _, _ = timed(degraded_e2e, skip_d, args.steps, e2e=True, graph=use_graph)
     e2e_value = tokens_per_step * args.steps / (ms_e2e / 1000.0)
     h2d = sum(2 * mb.tokens.numel() * 8 for mb in degraded_e2e)
     loss_ok = bool(torch.isfinite(eng.losses).all().item())
@@ -362,7 +394,10 @@ def main():
         "drop_pct_instantaneous": round(100.0 * (1.0 - value / ff_value), 2) if ff_value else None,
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4 * R},
-        "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
+        "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
+        "profiled_kernel_ms_per_step": round(kernel_ms / args.steps, 3),
+        "gpu_busy_frac_eager": round(kernel_ms / ms_prof, 4), "ms_per_step_eager_profiled": round(ms_prof / args.steps, 3),
+        "launch_mode": "cuda_graph" if use_graph else "eager", "cpu_baseline": cpu,
         "clocks": clk.summary(), "loss_finite": loss_ok, "wall_s_timed": round(wall, 3),
     }
     print(json.dumps(out), flush=True)

@@ -78,7 +78,17 @@ class ProjectionCache:
     def set_basis(self, kind: str, v1) -> None:
         """Inject a basis (e.g. the reference's seeded V1 for parity)."""
         t = torch.as_tensor(v1).to("cuda", torch.float32).contiguous()
+        old = self.basis.get(kind)
         self.basis[kind] = t
+        if old is not None and tuple(old.shape) == tuple(t.shape):
+            # refresh in place: packed engine operands keep their addresses
+            # (captured CUDA graphs read them by pointer)
+            for (prec, rp), (_, keep) in self._packed.items():
+                v, vt = keep[1 + 2 * FFN_KINDS.index(kind)], keep[2 + 2 * FFN_KINDS.index(kind)]
+                v.zero_()
+                v[:, :t.shape[1]] = t.to(v.dtype)
+                vt.copy_(v.t())
+            return
         self._packed.clear()
 
     def packed(self, precision: str):

@@ -84,6 +84,7 @@ class StepEngine:
         self.projs: dict = {}
         self._keep = []
         self.losses = None
+        self.graphs = []
 
     # ------------------------------------------------------------------ utils
     def _gp(self, name: str) -> int:
@@ -165,12 +166,44 @@ class StepEngine:
         _lib.call("mecefo_embedding_backward", eng.handle, self.tok.data_ptr(), self.dx[cur].data_ptr(),
                   self._gp("embedding"), mb.alpha_global, b, s)
 
+    # ------------------------------------------------------------ optimizer
+    def _seg_slot(self, slot: int, nseg: int):
+        """Pinned host + device segment tables (two slots: one step of host
+        look-ahead without racing the copy of the previous step)."""
+        if not hasattr(self, "_segs"):
+            n = len(self.weights.layout)
+            nbytes = n * ctypes.sizeof(_lib.AdamSegment)
+            self._segs = [(torch.empty(nbytes, dtype=torch.uint8).pin_memory(),
+                           torch.empty(nbytes, dtype=torch.uint8, device=self.device),
+                           torch.cuda.Event()) for _ in range(2)]
+            self._seg_k = 0
+        return self._segs[slot]
+
+    def _adam_launch(self, lr: float, skip, slot: int, stream_ptr: int, fill: bool = True,
+                     record: bool = True) -> None:
+        host, dev, ev = self._seg_slot(slot, 0)
+        if fill:
+            ev.synchronize()  # the copy that last read this slot has executed
+            arr, max_numel, names = op.adam_segments(self.weights, self.opt, lr, skip)
+            host.numpy()[: arr.nbytes] = arr.view(np.uint8)
+            for name in names:
+                self.opt.step[name] = self.opt.step.get(name, 0) + 1
+            self._adam_meta = (len(names), max_numel)
+        nseg, max_numel = self._adam_meta
+        dev.copy_(host, non_blocking=True)
+        if record:
+            ev.record()
+        if nseg:
+            cfg = self.opt.cfg
+            shadow = self.weights.shadow.data_ptr() if self.precision != "fp32" else None
+            _lib.call("mecefo_adamw_step", self.eng.handle, dev.data_ptr(), nseg, max_numel,
+                      self.weights.master.data_ptr(), self.grad.data_ptr(), self.opt.m.data_ptr(),
+                      self.opt.v.data_ptr(), shadow, cfg.beta1, cfg.beta2, cfg.eps, stream_ptr)
+
     # ---------------------------------------------------------------- step
-    def step(self, mbs: list, n_ranks: int, lr: float, skip=(), check: bool = True) -> torch.Tensor:
-        """Run this GPU's microbatches, exchange, update. Returns the (n_ranks,)
-        device vector of per-rank losses (all-reduced across processes)."""
+    def _body(self, mbs: list, losses: torch.Tensor) -> None:
         self.grad.zero_()
-        losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
+        losses.zero_()
         for mb in mbs:
             self.microbatch(mb, losses.data_ptr() + 4 * mb.rank)
         if self.group is not None:
@@ -178,9 +211,74 @@ class StepEngine:
 
             dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
             dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=self.group)
-        op.apply_flat(self.weights, self.opt, self.grad, lr, skip=skip, check=check)
-        self.losses = losses
-        return losses
+
+    def step(self, mbs: list, n_ranks: int, lr: float, skip=(), check: bool = True) -> torch.Tensor:
+        """Run this GPU's microbatches, exchange, update (eager launches).
+        Returns the (n_ranks,) device vector of per-rank losses."""
+        if self.losses is None or self.losses.numel() != n_ranks:
+            self.losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
+        self._body(mbs, self.losses)
+        if check:
+            op.apply_flat(self.weights, self.opt, self.grad, lr, skip=skip, check=True)
+        else:
+            self.opt.ensure_flat(self.weights.total, self.device)
+            slot = self._seg_k = (getattr(self, "_seg_k", 0) + 1) % 2
+            self._adam_launch(lr, skip, slot, runtime.stream_ptr())
+        return self.losses
+
+    def capture(self, mbs: list, n_ranks: int, skip=()) -> None:
+        """Capture one whole iteration (both microbatches' forward/backward,
+        the Eq. (1) all-reduce and the fused AdamW) as CUDA graphs, one per
+        optimizer-segment slot. Call after an eager step with the same plan
+        (projections refreshed, descriptors and kernel attributes warm)."""
+        if self.losses is None or self.losses.numel() != n_ranks:
+            self.losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
+        self._seg_slot(0, 0)
+        arr, max_numel, names = op.adam_segments(self.weights, self.opt, 1e-4, skip)
+        self._adam_meta = (len(names), max_numel)
+        self._graph_plan = (list(mbs), n_ranks, tuple(skip))
+        torch.cuda.synchronize()
+        steps = {k: pc.step for k, pc in self.projs.items()}
+        self.graphs = []
+        for slot in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body(mbs, self.losses)
+                self._adam_launch(0.0, skip, slot, runtime.stream_ptr(), fill=False, record=False)
+            self.graphs.append(g)
+        for k, v in steps.items():  # capture ran the host bookkeeping once; undo it
+            self.projs[k].step = v
+        torch.cuda.synchronize()
+
+    def replay(self, lr: float) -> torch.Tensor:
+        """One captured iteration: host bookkeeping (optimizer scalars,
+        projection step counters) then a single graph launch."""
+        mbs, n_ranks, skip = self._graph_plan
+        slot = self._seg_k = (getattr(self, "_seg_k", 0) + 1) % 2
+        host, dev, ev = self._segs[slot]
+        ev.synchronize()
+        arr, _, names = op.adam_segments(self.weights, self.opt, lr, skip)
+        host.numpy()[: arr.nbytes] = arr.view(np.uint8)
+        for name in names:
+            self.opt.step[name] = self.opt.step.get(name, 0) + 1
+        for mb in mbs:
+            for l in range(self.cfg.layers):
+                if mb.lean[l]:
+                    self.proj(mb.rank, l).step += 1
+        self.graphs[slot].replay()
+        ev.record()
+        return self.losses
+
+    def projections_due(self, mbs: list) -> bool:
+        """True if any lean layer's projection refresh is due next iteration
+        (approx.py:74-75); graph replay must then fall back to an eager step."""
+        for mb in mbs:
+            for l in range(self.cfg.layers):
+                if mb.lean[l]:
+                    pc = self.proj(mb.rank, l)
+                    if not pc.basis or pc.step % pc.refresh_period == 0:
+                        return True
+        return False
 
 
 def ring_plan(n_ranks: int, failed, layers: int, gpu_of_rank=None):

@@ -1,0 +1,135 @@
+"""GPU: the fused step engine (flat Eq. (1)-weighted gradient buffer, fused
+AdamW, CUDA-graph replay) against the oracle's per-rank rank passes plus the
+reference aggregation (cluster.py:292-322) and AdamW (optim.py:75-103)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cluster_ref, model_ref as R, optim_ref
+from paper_2510_16415_b200 import engine as E, model as mdl
+
+pytestmark = pytest.mark.gpu
+
+C0 = mdl.ModelConfig(vocab=64, hidden=128, heads=4, ffn_intermediate=344, layers=2, seq_len=64)
+D0 = R.Dims(64, 128, 4, 344, 2, 64)
+
+
+def _batches(n_ranks, seqs, seed=0):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return [(rng.integers(0, 64, size=(seqs, 64)), rng.integers(0, 64, size=(seqs, 64))) for _ in range(n_ranks)]
+
+
+def _engine(prec, seqs):
+    eng = E.StepEngine(C0, precision=prec, seqs_per_microbatch=seqs, r=32, tau=10**6)
+    rng = np.random.Generator(np.random.PCG64(11))
+    bases = {}
+    for j in range(4):
+        for l in range(2):
+            pc = eng.proj(j, l)
+            bl = {k: np.linalg.qr(rng.normal(size=(n, 32)))[0] for k, n in (("gate", 128), ("up", 128),
+                                                                              ("down", 344))}
+            for k, v in bl.items():
+                pc.set_basis(k, v)
+            pc.step = 1  # injected: no refresh due
+            bases[(j, l)] = bl
+    return eng, bases
+
+
+def _plan(R_, failed, batches):
+    route, lean, a_mha, skip = E.ring_plan(R_, set(failed), 2)
+    mbs = []
+    for j in range(R_):
+        tk, tg = batches[j]
+        mbs.append(E.Microbatch(rank=j, tokens=torch.from_numpy(tk).cuda(), targets=torch.from_numpy(tg).cuda(),
+                                lean=[lean[j]] * 2, alpha_mha=[None if lean[j] else a_mha] * 2, alpha_ffn=1.0 / R_,
+                                alpha_global=1.0 / R_))
+    return mbs, lean, skip
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("bf16", 5e-2)])
+@pytest.mark.parametrize("R_,failed", [(2, {1}), (4, {2}), (3, ())])
+def test_eq1_weighted_gradients_match_reference_aggregation(cuda, prec, tol, R_, failed):
+    batches = _batches(R_, 2)
+    eng, bases = _engine(prec, 2)
+    mbs, lean, skip = _plan(R_, failed, batches)
+    losses = torch.zeros(R_, device="cuda")
+    eng._body(mbs, losses)  # all ranks on this GPU: the local flat buffer is the full Eq. (1) sum
+    torch.cuda.synchronize()
+    W = R.init_params(D0, 0)
+    per_rank, ref_losses = [], []
+    for j in range(R_):
+        modes = ["ffn_input_only" if lean[j] else "full"] * 2
+        loss, g = R.rank_pass(D0, W, batches[j][0], batches[j][1], modes,
+                              {l: bases[(j, l)] for l in range(2)} if lean[j] else None)
+        per_rank.append(g)
+        ref_losses.append(loss)
+    active = {(l, k): ([j for j in range(R_) if not lean[j]] if k in cluster_ref.MHA else list(range(R_)))
+              for l in range(2) for k in cluster_ref.MHA + cluster_ref.FFN}
+    avg, skipped = cluster_ref.aggregate(per_rank, active, 2)
+    assert sorted(skipped) == sorted(skip)
+    assert np.allclose(losses.cpu().numpy(), ref_losses, rtol=tol, atol=tol)
+    for name, shape, off in eng.weights.layout:
+        got = eng.grad[off: off + int(np.prod(shape))].view(shape).cpu().numpy()
+        if name in skipped:
+            assert not got.any(), name  # never accumulated (select, not multiply)
+        else:
+            assert R.rel_err(got, avg[name]) < tol, name
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("bf16", 5e-2)])
+def test_step_with_adamw_matches_reference(cuda, prec, tol):
+    batches = _batches(2, 2, seed=3)
+    eng, bases = _engine(prec, 2)
+    mbs, lean, skip = _plan(2, {1}, batches)
+    W = R.init_params(D0, 0)
+    opt = optim_ref.Adam()
+    for it in range(3):
+        lr = optim_ref.lr_at(it + 1, 3, 1e-3)
+        eng.step(mbs, 2, lr, skip=skip, check=True)
+        per_rank = [R.rank_pass(D0, W, batches[j][0], batches[j][1], ["ffn_input_only"] * 2,
+                                {l: bases[(j, l)] for l in range(2)})[1] for j in range(2)]
+        active = {(l, k): ([] if k in cluster_ref.MHA else [0, 1]) for l in range(2)
+                  for k in cluster_ref.MHA + cluster_ref.FFN}
+        avg, skipped = cluster_ref.aggregate(per_rank, active, 2)
+        opt.apply(W, avg, lr, skip=skipped)
+    # Adam normalises each element's update to ~lr, so an element whose tiny
+    # gradient flips sign under fp32 rounding moves by ~2 lr: bound the weight
+    # error by the update scale, and require almost all elements to agree.
+    W0 = R.init_params(D0, 0)
+    for name, t in eng.weights.named():
+        if name in skipped:
+            continue  # checked exactly below
+        got = t.cpu().numpy().astype(np.float64)
+        err = np.abs(got - W[name])
+        step = np.abs(W[name] - W0[name]).max() + 1e-6 * np.abs(W0[name]).max()  # + fp32 rounding of w
+        assert err.max() <= 2.5 * step, name
+        frac_bad = float((err > (1e-4 if prec == "fp32" else 3e-2) * step).mean())
+        assert frac_bad < (1e-2 if prec == "fp32" else 1e-1), (name, frac_bad)
+    # skipped MHA params never moved, and their step counters never advanced
+    assert np.array_equal(eng.weights.get("layers.0.q").cpu().numpy(),
+                          R.init_params(D0, 0)["layers.0.q"].astype(np.float32))
+    assert "layers.0.q" not in eng.opt.step and eng.opt.step["layers.0.gate"] == 3
+
+
+def test_graph_replay_matches_eager(cuda):
+    batches = _batches(2, 2, seed=5)
+    outs = []
+    for graph in (False, True):
+        eng, _ = _engine("bf16", 2)
+        mbs, lean, skip = _plan(2, {1}, batches)
+        eng.step(mbs, 2, 1e-3, skip=skip, check=False)
+        if graph:
+            eng.capture(mbs, 2, skip)
+        for _ in range(3):
+            if graph:
+                eng.replay(1e-3)
+            else:
+                eng.step(mbs, 2, 1e-3, skip=skip, check=False)
+        torch.cuda.synchronize()
+        outs.append((eng.weights.master.clone(), eng.losses.clone(), dict(eng.opt.step),
+                     {k: pc.step for k, pc in eng.projs.items()}))
+    (w0, l0, s0, p0), (w1, l1, s1, p1) = outs
+    assert s0 == s1 and p0 == p1
+    assert torch.allclose(l0, l1, rtol=1e-3, atol=1e-4)
+    assert R.rel_err(w0.cpu().numpy(), w1.cpu().numpy()) < 1e-3
