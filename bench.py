@@ -374,6 +374,7 @@ def main():
     loss_ok = bool(torch.isfinite(eng.losses).all().item())
 
     if rank != 0:
+        _finish(group, eng)
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -401,8 +402,24 @@ def main():
         "clocks": clk.summary(), "loss_finite": loss_ok, "wall_s_timed": round(wall, 3),
     }
     print(json.dumps(out), flush=True)
-    if group is not None:
-        dist.destroy_process_group()
+    _finish(group, eng)
+
+
+def _finish(group, eng):
+    """Multi-process teardown: drop the captured graphs (they hold NCCL work),
+    synchronize, meet at a barrier and exit without destroying the NCCL
+    communicator (its destruction with graph-captured collectives can hang)."""
+    if group is None:
+        return
+    import torch
+    import torch.distributed as dist
+
+    eng.graphs = []
+    torch.cuda.synchronize()
+    dist.barrier()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
 
 
 if __name__ == "__main__":
