@@ -164,6 +164,26 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def _profile_records(lib):
+    """Aggregate the engine's launch-profiler records by tag and stop it."""
+    import ctypes
+
+    from paper_2510_16415_b200 import _lib
+
+    agg = {}
+    for i in range(lib.mecefo_profile_count()):
+        tag, kms, fl, by = ctypes.c_char_p(), ctypes.c_float(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(lib.mecefo_profile_record(i, ctypes.byref(tag), ctypes.byref(kms), ctypes.byref(fl),
+                                             ctypes.byref(by)))
+        a = agg.setdefault(tag.value.decode(), [0.0, 0, 0.0, 0.0])
+        a[0] += kms.value
+        a[1] += 1
+        a[2] += fl.value
+        a[3] += by.value
+    lib.mecefo_profile_enable(0)
+    return agg
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -311,23 +331,7 @@ def main():
     ms_eager = ms_prof
 
     # dominant kernel roofline from the live profile of the timed region
-    n = lib.mecefo_profile_count()
-    import ctypes
-
-    agg = {}
-    for i in range(n):
-        tag = ctypes.c_char_p()
-        kms = ctypes.c_float()
-        fl = ctypes.c_double()
-        by = ctypes.c_double()
-        _lib.check(lib.mecefo_profile_record(i, ctypes.byref(tag), ctypes.byref(kms), ctypes.byref(fl),
-                                             ctypes.byref(by)))
-        a = agg.setdefault(tag.value.decode(), [0.0, 0, 0.0, 0.0])
-        a[0] += kms.value
-        a[1] += 1
-        a[2] += fl.value
-        a[3] += by.value
-    lib.mecefo_profile_enable(0)
+    agg = _profile_records(lib)
     hbm, bf16, bf16_sus, peak_src = _peaks()
     top = sorted(agg.items(), key=lambda kv: -kv[1][0])
     roofline = None
@@ -355,6 +359,7 @@ def main():
 
     # fault-free step (every GPU one exact microbatch) and instantaneous drop
     ff_value = None
+    kernels_ff = None
     if not args.no_fault_free:
         for _ in range(2):
             eng.step(fault_free, R, lr, skip=skip_f, check=False)
@@ -362,6 +367,10 @@ def main():
             capture(fault_free, skip_f)
         ms_ff, _, _ = timed(fault_free, skip_f, args.steps, graph=use_graph)
         ff_value = tokens_per_step * args.steps / (ms_ff / 1000.0)
+        ms_ffp, _, _ = timed(fault_free, skip_f, args.steps, profile=True)
+        agg_ff = _profile_records(lib)
+        kernels_ff = [{"tag": t, "ms_per_step": round(v[0] / args.steps, 3), "share": round(v[0] / ms_ffp, 4)}
+                      for t, v in sorted(agg_ff.items(), key=lambda kv: -kv[1][0])[:10]]
 
     # end-to-end through the public API: H2D of inputs + D2H of the loss per step
     if use_graph:
@@ -392,6 +401,7 @@ def main():
                    "parallelism": f"dp{world} (MeCeFO ring, NDB neighbour)", "l2": "inputs larger than L2 "
                    "(per-step activations + logits > 126 MB)", "refresh_period": 100},
         "fault_free_tokens_per_s": round(ff_value, 1) if ff_value else None,
+        "kernels_fault_free": kernels_ff,
         "drop_pct_instantaneous": round(100.0 * (1.0 - value / ff_value), 2) if ff_value else None,
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4 * R},
