@@ -16,6 +16,7 @@
 #include "../../include/mecefo.h"
 #include "attention.cuh"
 #include "attention_tc.cuh"
+#include "attention_bwd_tc.cuh"
 #include "gemm_dual.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
@@ -516,6 +517,20 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
     dim3 grid((unsigned)(tokens / a.T) * a.H, (unsigned)((a.T + 127) / 128));
     attn_fwd_tc_kernel<<<grid, ATC_THREADS, ATC_SMEM, s>>>(tq, t);
     return check_launch("attn_fwd_tc_kernel");
+  }
+  if (backward && e->prec == PREC_BF16 && hd == 64 && a.T % 128 == 0 && a.T <= 256) {
+    ProfScope prof("attn_bwd_tc", 5.0 * tokens * a.T * a.m, (double)tokens * a.m * e->ps * 9, s);
+    CUtensorMap tq, tdo;
+    TRY(make_tmap(e, &tq, a.qkv, 3 * a.m, tokens, a.ld_qkv, 64, 64));
+    TRY(make_tmap(e, &tdo, a.dctx, a.m, tokens, a.ld_ctx, 64, 64));
+    AttnBwdTcArgs t{a.ctx, a.dctx, a.lse, a.dqkv, a.cosT, a.sinT, a.T, a.H, a.m, a.rope, a.scale};
+    static bool set = false;
+    if (!set) {
+      CUDA_TRY(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ABT_SMEM));
+      set = true;
+    }
+    attn_bwd_tc_kernel<<<(unsigned)((tokens / a.T) * a.H), ABT_THREADS, ABT_SMEM, s>>>(tq, tdo, t);
+    return check_launch("attn_bwd_tc_kernel");
   }
   ProfScope prof(backward ? "attn_bwd" : "attn_fwd", (backward ? 4.0 : 2.0) * tokens * a.T * a.m,
                  (double)tokens * a.m * e->ps * (backward ? 9 : 4), s);

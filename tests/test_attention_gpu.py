@@ -47,10 +47,12 @@ def test_forward_block_hd64(cuda, prec, tol, T, seqs):
 
 
 @pytest.mark.parametrize("prec,tol", [("bf16", BF16_TOL), ("fp32", 1e-4)])
-def test_exact_backward_hd64(cuda, prec, tol):
-    cfg, d, W, x, dy = _setup(seqs=2)
-    _, c_ref = R.block_fwd(d, W, 0, x.reshape(2, 256, -1), lean=False)
-    dx_ref, g_ref = R.block_bwd_exact(d, W, 0, c_ref, dy.reshape(2, 256, -1))
+@pytest.mark.parametrize("T,seqs", [(256, 2), (128, 3)])
+def test_exact_backward_hd64(cuda, prec, tol, T, seqs):
+    """bf16: tcgen05 attention backward (T in {128, 256}); fp32: SIMT path."""
+    cfg, d, W, x, dy = _setup(T=T, seqs=seqs)
+    _, c_ref = R.block_fwd(d, W, 0, x.reshape(seqs, T, -1), lean=False)
+    dx_ref, g_ref = R.block_bwd_exact(d, W, 0, c_ref, dy.reshape(seqs, T, -1))
     w = mdl.init_weights(cfg, 0, precision=prec)
     _, cache = mdl.forward_block(cfg, w.layers[0], torch.tensor(x, dtype=torch.float32, device="cuda"),
                                  mdl.CACHE_FULL)
