@@ -212,6 +212,7 @@ struct GemmCall {
   Epilogue epi{};
   int split = 1;
   const char* tag = "gemm";
+  int force_bn = 0;  // tcgen05 tile width override (split-K accumulate GEMMs)
 };
 
 Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, float beta = 0.f,
@@ -305,6 +306,7 @@ int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
 // pick the BN minimising it, and on ties the widest (better L2 arithmetic
 // intensity: 128x256 tiles read 85 flop/B, 128x64 only 51).
 int choose_bn(const GemmCall& g) {
+  if (g.force_bn) return g.force_bn;
   const int64_t nacc = g.paired ? 2 * g.N : g.N;
   const int64_t tm = (g.M + 127) / 128;
   // per-flop penalty of narrower tiles (L2-bound operand traffic), measured
@@ -368,8 +370,13 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
 // out (fp32, ldo) += alpha * A B^T; split-K with atomics when the output has
 // too few tiles to fill the GPU (the long-K Wgrad / low-rank contractions).
 int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float alpha, cudaStream_t s) {
-  const int tiles = tiles_for(g, e->prec);
   const int kblocks = (int)((g.K + 63) / 64);
+  if (e->prec == PREC_BF16 && kblocks >= 8 && ((g.M + 127) / 128) * ((g.N + 255) / 256) < kNumSMs / 2) {
+    // long-K, small output: one N tile as wide as the output (each A element
+    // read once), split K across the SMs
+    g.force_bn = g.N > 128 ? 256 : (g.N > 64 ? 128 : 64);
+  }
+  const int tiles = tiles_for(g, e->prec);
   if (tiles < 2 * kNumSMs / 3 && kblocks >= 8) {
     Epilogue ep{};
     ep.kind = EPI_ATOMIC; ep.out = out; ep.ldo = ldo; ep.alpha = alpha; ep.out_prec = PREC_F32;
@@ -458,7 +465,7 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
     TRY(check_launch("rmsnorm_bwd_kernel"));
   }
   if (grad_scale) {
-    colsum_finalize_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(partial, nblk, (int)m, grad_scale, alpha, 1.f);
+    colsum_finalize_kernel<<<(unsigned)((m + 31) / 32), 256, 0, s>>>(partial, nblk, (int)m, grad_scale, alpha, 1.f);
     TRY(check_launch("colsum_finalize_kernel"));
   }
   return MECEFO_OK;
@@ -1197,11 +1204,13 @@ int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t
                       void* stream) {
   if (nseg <= 0) return MECEFO_OK;
   static_assert(sizeof(mecefo_adam_segment) == sizeof(AdamSeg), "segment layout");
-  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((max_numel + 255) / 256, 64));
-  dim3 grid((unsigned)bx, (unsigned)nseg);
-  adamw_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const AdamSeg*>(segs), nseg, w, grad, m1, m2, shadow, e ? e->prec : PREC_F32, beta1, beta2,
-      eps);
+  (void)max_numel;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  ProfScope prof("adamw", 0.0, 0.0, s);
+  const unsigned grid = 8 * kNumSMs;  // grid-stride over the concatenated active segments
+  adamw_kernel<<<grid, 256, (nseg + 1) * sizeof(int64_t), s>>>(reinterpret_cast<const AdamSeg*>(segs), nseg, w, grad,
+                                                               m1, m2, shadow, e ? e->prec : PREC_F32, beta1, beta2,
+                                                               eps);
   return check_launch("adamw_kernel");
 }
 

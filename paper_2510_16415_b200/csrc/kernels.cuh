@@ -100,13 +100,23 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const float* __r
 }
 
 // out[c] = beta*out[c] + alpha * sum_b partial[b, c] (fixed order over b).
+// Block (32 x 8): 32 columns, 8 row-strided partial sums each, fixed order.
 __global__ void colsum_finalize_kernel(const float* __restrict__ partial, int nblocks, int m, float* __restrict__ out,
                                        float alpha, float beta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= m) return;
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
   float t = 0.f;
-  for (int b = 0; b < nblocks; ++b) t += partial[(int64_t)b * m + c];
-  out[c] = (beta != 0.f ? beta * out[c] : 0.f) + alpha * t;
+  if (c < m)
+    for (int b = ty; b < nblocks; b += 8) t += partial[(int64_t)b * m + c];
+  red[ty][tx] = t;
+  __syncthreads();
+  if (ty == 0 && c < m) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][tx];
+    out[c] = (beta != 0.f ? beta * out[c] : 0.f) + alpha * s;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -208,15 +218,26 @@ struct AdamSeg {
   int pad;
 };
 
-__global__ void adamw_kernel(const AdamSeg* __restrict__ segs, int nseg, float* __restrict__ w,
-                             const float* __restrict__ grad, float* __restrict__ m1, float* __restrict__ m2,
-                             void* __restrict__ shadow, int shadow_prec, float beta1, float beta2, float eps) {
-  // blockIdx.y selects the segment; grid-stride over its elements.
-  const int s = blockIdx.y;
-  if (s >= nseg) return;
-  const AdamSeg sg = segs[s];
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < sg.numel; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = sg.offset + j;
+// The active segments are concatenated into one virtual range; every thread
+// updates 4 consecutive elements per iteration (float4 when aligned), so the
+// large embedding/unembedding segments spread over the whole GPU.
+__global__ void __launch_bounds__(256) adamw_kernel(const AdamSeg* __restrict__ segs, int nseg,
+                                                    float* __restrict__ w, const float* __restrict__ grad,
+                                                    float* __restrict__ m1, float* __restrict__ m2,
+                                                    void* __restrict__ shadow, int shadow_prec, float beta1,
+                                                    float beta2, float eps) {
+  extern __shared__ int64_t cum[];  // nseg + 1 prefix sums of numel
+  if (threadIdx.x == 0) {
+    int64_t c = 0;
+    for (int s = 0; s < nseg; ++s) {
+      cum[s] = c;
+      c += segs[s].numel;
+    }
+    cum[nseg] = c;
+  }
+  __syncthreads();
+  const int64_t total = cum[nseg];
+  auto upd = [&](const AdamSeg& sg, int64_t i) {
     const float g = grad[i];
     float mm = m1[i], vv = m2[i];
     mm = beta1 * mm + (1.f - beta1) * g;
@@ -224,10 +245,52 @@ __global__ void adamw_kernel(const AdamSeg* __restrict__ segs, int nseg, float* 
     m1[i] = mm;
     m2[i] = vv;
     const float wi = w[i];
-    const float upd = sg.step_size * mm / (sqrtf(vv * sg.inv_bc2) + eps) + sg.lr_wd * wi;
-    const float wn = wi - upd;
+    const float wn = wi - (sg.step_size * mm / (sqrtf(vv * sg.inv_bc2) + eps) + sg.lr_wd * wi);
     w[i] = wn;
     if (shadow) store_from_f32(shadow, i, wn, shadow_prec);
+  };
+  for (int64_t v = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); v < total;
+       v += 4 * (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nseg - 1;  // last segment with cum[s] <= v
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cum[mid] <= v) lo = mid; else hi = mid - 1;
+    }
+    const AdamSeg sg = segs[lo];
+    const int64_t i = sg.offset + (v - cum[lo]);
+    if (v + 4 <= cum[lo + 1] && (i & 3) == 0) {
+      const float4 g = *reinterpret_cast<const float4*>(grad + i);
+      float4 mm = *reinterpret_cast<const float4*>(m1 + i), vv = *reinterpret_cast<const float4*>(m2 + i);
+      float4 wi = *reinterpret_cast<const float4*>(w + i);
+      float gg[4] = {g.x, g.y, g.z, g.w}, ma[4] = {mm.x, mm.y, mm.z, mm.w}, va[4] = {vv.x, vv.y, vv.z, vv.w};
+      float wa[4] = {wi.x, wi.y, wi.z, wi.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ma[q] = beta1 * ma[q] + (1.f - beta1) * gg[q];
+        va[q] = beta2 * va[q] + (1.f - beta2) * (gg[q] * gg[q]);
+        wa[q] = wa[q] - (sg.step_size * ma[q] / (sqrtf(va[q] * sg.inv_bc2) + eps) + sg.lr_wd * wa[q]);
+      }
+      *reinterpret_cast<float4*>(m1 + i) = make_float4(ma[0], ma[1], ma[2], ma[3]);
+      *reinterpret_cast<float4*>(m2 + i) = make_float4(va[0], va[1], va[2], va[3]);
+      *reinterpret_cast<float4*>(w + i) = make_float4(wa[0], wa[1], wa[2], wa[3]);
+      if (shadow) {
+        if (shadow_prec == PREC_BF16) {
+          __nv_bfloat162 a = __floats2bfloat162_rn(wa[0], wa[1]), b = __floats2bfloat162_rn(wa[2], wa[3]);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&a);
+          u.y = *reinterpret_cast<uint32_t*>(&b);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(shadow) + i) = u;
+        } else {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(shadow) + i) = make_float4(wa[0], wa[1], wa[2], wa[3]);
+        }
+      }
+    } else {
+      for (int q = 0; q < 4 && v + q < total; ++q) {
+        int s = lo;
+        while (v + q >= cum[s + 1]) ++s;
+        upd(segs[s], segs[s].offset + (v + q - cum[s]));
+      }
+    }
   }
 }
 
