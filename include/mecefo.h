@@ -188,6 +188,12 @@ int mecefo_head_logits(mecefo_engine* e, const float* x_last, const float* final
 int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens, float* loss,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* cross_entropy over `tokens / group_rows` stacked microbatches (logical
+ * ranks) at once: each group's dlogits are scaled by 1/group_rows and
+ * loss[g] is group g's mean, exactly as separate per-rank calls. */
+int mecefo_cross_entropy_grouped(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens,
+                                 int64_t group_rows, float* loss, void* ws, size_t ws_bytes, void* stream);
+
 /* model.py:476-483 head_backward (+ accumulate into g_final_norm/g_unemb). */
 int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* final_norm, const float* inv_f,
                          const void* xf, const void* dlogits, const void* unemb_c, float* dx, void* dx_c,

@@ -68,16 +68,21 @@ class ProjectionCache:
     basis: dict = field(default_factory=dict)
     svd_calls: int = 0
     refreshes: int = 0
+    # provenance of the current basis: equal tokens <=> bitwise-equal bases
+    # (lets the engine fuse microbatches whose ranks share a basis)
+    token: object = None
     _packed: dict = field(default_factory=dict, repr=False)
 
     def reset(self) -> None:
         self.step = 0
         self.basis.clear()
         self._packed.clear()
+        self.token = None
 
     def set_basis(self, kind: str, v1) -> None:
         """Inject a basis (e.g. the reference's seeded V1 for parity)."""
         t = torch.as_tensor(v1).to("cuda", torch.float32).contiguous()
+        self.token = ("inject", object())
         old = self.basis.get(kind)
         self.basis[kind] = t
         if old is not None and tuple(old.shape) == tuple(t.shape):

@@ -62,6 +62,7 @@ __device__ void stage_rows(float* dst, const void* src, int64_t ld, int64_t row_
 
 template <int D>
 __global__ void __launch_bounds__(256) attn_fwd_kernel(AttnDev a) {
+  griddep_wait();
   extern __shared__ float sm[];
   const int bh = blockIdx.x, seq = bh / a.H, h = bh % a.H;
   const int q0 = blockIdx.y * 64;
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(AttnDev a) {
 // dQ (and rowsum(dO*O)) for a block of 64 query rows.
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(AttnDev a) {
+  griddep_wait();
   extern __shared__ float sm[];
   const int bh = blockIdx.x, seq = bh / a.H, h = bh % a.H;
   const int q0 = blockIdx.y * 64;
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(AttnDev a) {
 // dK, dV for a block of 64 key rows (queries i >= j).
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_dkv_kernel(AttnDev a) {
+  griddep_wait();
   extern __shared__ float sm[];
   const int bh = blockIdx.x, seq = bh / a.H, h = bh % a.H;
   const int k0 = blockIdx.y * 64;

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(ABT_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  griddep_wait();  // predecessor outputs are visible from here on
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 

@@ -30,6 +30,11 @@ __device__ __forceinline__ void store_from_f32(void* p, int64_t i, float v, int 
     reinterpret_cast<float*>(p)[i] = v;
 }
 
+// Programmatic dependent launch: every engine kernel is launched with
+// programmatic stream serialization, so it may start while its predecessor is
+// still draining; it must wait here before touching the predecessor's output.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -12,6 +13,7 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <utility>
 
 #include "../../include/mecefo.h"
 #include "attention.cuh"
@@ -102,6 +104,31 @@ struct ProfScope {
     if (idx < (int64_t)g_prof.recs.size()) cudaEventRecord(g_prof.recs[idx].b, s);
   }
 };
+
+// Every engine kernel goes out with programmatic stream serialization (PDL):
+// it may be scheduled while its predecessor drains, runs its prologue
+// (barrier init, TMEM alloc, descriptor prefetch) and blocks in
+// griddepcontrol.wait until the predecessor's results are visible. Kept in
+// CUDA-graph capture as programmatic edges. MECEFO_NO_PDL=1 disables it.
+bool pdl_enabled() {
+  static const bool on = getenv("MECEFO_NO_PDL") == nullptr;
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Bump allocator over the caller's workspace.
 struct Ws {
@@ -224,14 +251,14 @@ Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, floa
   return e;
 }
 
-template <int BN, bool AK, bool BKM>
+template <int BN, bool AK, bool BKM, int CL>
 int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   using C = TcCfg<BN>;
   CUtensorMap ta, tb;
   if (AK) TRY(make_tmap(e, &ta, g.a.p, g.K, g.M, g.a.ld, 64, TC_BM));
   else TRY(make_tmap(e, &ta, g.a.p, g.M, g.K, g.a.ld, 64, 64));
   const int64_t rowsB = g.paired ? g.pair_off + g.N : g.N;
-  if (BKM) TRY(make_tmap(e, &tb, g.b.p, g.K, rowsB, g.b.ld, 64, g.paired ? BN / 2 : BN));
+  if (BKM) TRY(make_tmap(e, &tb, g.b.p, g.K, rowsB, g.b.ld, 64, (g.paired || CL > 1) ? BN / 2 : BN));
   else TRY(make_tmap(e, &tb, g.b.p, rowsB, g.K, g.b.ld, 64, 64));
   GemmDev p{};
   p.M = (int)g.M; p.N = (int)g.N; p.K = (int)g.K;
@@ -245,6 +272,8 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   const int cols_per_tile = g.paired ? BN / 2 : BN;
   p.tiles_n = (int)((g.N + cols_per_tile - 1) / cols_per_tile);
   p.num_tiles = p.tiles_m * p.tiles_n * p.split;
+  p.tiles_m_cl = (p.tiles_m + CL - 1) / CL;
+  p.num_tiles_cl = p.tiles_m_cl * p.tiles_n * p.split;
   p.epi = g.epi;
   // output slots -> TMA store / reduce-add maps (32 x 32 boxes, swizzled)
   TcOut outs{};
@@ -283,22 +312,52 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     outs.prec[k] = slots[k].prec;
     outs.reduce[k] = slots[k].reduce;
   }
+  auto kern = gemm_tc_kernel<BN, AK, BKM, CL>;
   static bool attr_set = false;
   if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<BN, AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
-  const int grid = std::min(p.num_tiles, kNumSMs);
-  gemm_tc_kernel<BN, AK, BKM><<<grid, TC_THREADS, C::SMEM, s>>>(ta, tb, to[0], to[1], to[2], p, outs);
-  return check_launch("gemm_tc_kernel");
+  const int grid = CL * std::min(p.num_tiles_cl, kNumSMs / CL);
+  if (CL == 1) {
+    CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, ta, tb, to[0], to[1], to[2], p, outs));
+    return check_launch("gemm_tc_kernel");
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to[0], to[1], to[2], p, outs));
+  return check_launch("gemm_tc_kernel<cluster>");
 }
 
-template <int BN>
+template <int BN, int CL>
 int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
-  if (g.a.km && g.b.km) return launch_tc<BN, true, true>(e, g, s);
-  if (g.a.km && !g.b.km) return launch_tc<BN, true, false>(e, g, s);
-  if (!g.a.km && g.b.km) return launch_tc<BN, false, true>(e, g, s);
-  return launch_tc<BN, false, false>(e, g, s);
+  if (g.a.km && g.b.km) return launch_tc<BN, true, true, CL>(e, g, s);
+  if (g.a.km && !g.b.km) return launch_tc<BN, true, false, CL>(e, g, s);
+  if (!g.a.km && g.b.km) return launch_tc<BN, false, true, CL>(e, g, s);
+  return launch_tc<BN, false, false, CL>(e, g, s);
+}
+
+// TMA-multicast CTA pairs along M whenever there are at least two M tiles
+// and the B tile splits into halves (BN >= 128).
+// Measured: pays off only for very large tile counts (the LM-head GEMMs,
+// +10%); neutral-to-negative on the per-layer GEMMs.
+bool use_cluster(const GemmCall& g, int BN) {
+  if (getenv("MECEFO_NO_CLUSTER")) return false;
+  const int64_t cpt = g.paired ? BN / 2 : BN;
+  const int64_t tiles = ((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt);
+  return BN >= 128 && (g.M + 127) / 128 >= 2 && tiles >= 1024;
 }
 
 // Tile width for the tcgen05 path. The MMA time of a tile is proportional to
@@ -345,9 +404,10 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   if (e->prec == PREC_BF16) {
     if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
     const int BN = choose_bn(g);
-    if (BN == 256) return dispatch_tc_major<256>(e, g, s);
-    if (BN == 128) return dispatch_tc_major<128>(e, g, s);
-    return dispatch_tc_major<64>(e, g, s);
+    const bool cl = use_cluster(g, BN);
+    if (BN == 256) return cl ? dispatch_tc_major<256, 2>(e, g, s) : dispatch_tc_major<256, 1>(e, g, s);
+    if (BN == 128) return cl ? dispatch_tc_major<128, 2>(e, g, s) : dispatch_tc_major<128, 1>(e, g, s);
+    return dispatch_tc_major<64, 1>(e, g, s);
   }
   GemmDev p{};
   p.M = (int)g.M; p.N = (int)g.N; p.K = (int)g.K;
@@ -363,7 +423,7 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   SimtOperand A{g.a.p, g.a.ld, g.a.km ? 1 : 0, e->prec};
   SimtOperand B{g.b.p, g.b.ld, g.b.km ? 1 : 0, e->prec};
   dim3 grid(p.tiles_m, p.tiles_n, p.split);
-  gemm_simt_kernel<<<grid, 256, 0, s>>>(A, B, p);
+  CUDA_TRY(pdl_launch(gemm_simt_kernel, dim3(grid), dim3(256), 0, s, A, B, p));
   return check_launch("gemm_simt_kernel");
 }
 
@@ -393,7 +453,7 @@ int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float
 template <int NV>
 int launch_rms_fwd(const float* x, const float* g, void* out, float* inv, int64_t rows, int64_t m, int prec,
                    cudaStream_t s) {
-  rmsnorm_fwd_vec_kernel<NV><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(x, g, out, inv, (int)rows, (int)m, prec);
+  CUDA_TRY(pdl_launch(rmsnorm_fwd_vec_kernel<NV>, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, s, x, g, out, inv, (int)rows, (int)m, prec));
   return check_launch("rmsnorm_fwd_vec_kernel");
 }
 
@@ -409,8 +469,8 @@ int rmsnorm_fwd(mecefo_engine* e, const float* x, const float* g, void* out, flo
     return launch_rms_fwd<16>(x, g, out, inv, rows, m, e->prec, s);
   }
   const int warps = 8;
-  rmsnorm_fwd_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(x, g, out, inv, (int)rows, (int)m,
-                                                                                    e->prec);
+  CUDA_TRY(pdl_launch(rmsnorm_fwd_kernel, dim3((unsigned)((rows + warps - 1) / warps)), dim3(warps * 32), 0, s, x, g, out, inv, (int)rows, (int)m,
+                                                                                    e->prec));
   return check_launch("rmsnorm_fwd_kernel");
 }
 
@@ -423,8 +483,8 @@ int launch_rms_bwd(const float* x, const float* g, const float* inv, const float
     CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_vec_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     set = true;
   }
-  rmsnorm_bwd_vec_kernel<NV><<<nblk, 256, sm, s>>>(x, g, inv, d, resid, dx, dx_lp, prec, partial, (int)rows, (int)m,
-                                                   rpb);
+  CUDA_TRY(pdl_launch(rmsnorm_bwd_vec_kernel<NV>, dim3(nblk), dim3(256), sm, s, x, g, inv, d, resid, dx, dx_lp, prec, partial, (int)rows, (int)m,
+                                                   rpb));
   return check_launch("rmsnorm_bwd_vec_kernel");
 }
 
@@ -461,11 +521,11 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
       static bool set = false;
       if (!set) { CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); set = true; }
     }
-    rmsnorm_bwd_kernel<<<nblk, 256, sm, s>>>(x, g, inv, d, resid, dx, dx_lp, e->prec, partial, (int)rows, (int)m, rpb);
+    CUDA_TRY(pdl_launch(rmsnorm_bwd_kernel, dim3(nblk), dim3(256), sm, s, x, g, inv, d, resid, dx, dx_lp, e->prec, partial, (int)rows, (int)m, rpb));
     TRY(check_launch("rmsnorm_bwd_kernel"));
   }
   if (grad_scale) {
-    colsum_finalize_kernel<<<(unsigned)((m + 31) / 32), 256, 0, s>>>(partial, nblk, (int)m, grad_scale, alpha, 1.f);
+    CUDA_TRY(pdl_launch(colsum_finalize_kernel, dim3((unsigned)((m + 31) / 32)), dim3(256), 0, s, partial, nblk, (int)m, grad_scale, alpha, 1.f));
     TRY(check_launch("colsum_finalize_kernel"));
   }
   return MECEFO_OK;
@@ -498,14 +558,14 @@ int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const vo
     CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
     set = true;
   }
-  swiglu_bwd_dual_kernel<<<std::min(p.num_tiles, kNumSMs), TC_THREADS, DU_SMEM, s>>>(tdy, th2, twd, twgu, tact, tdg,
-                                                                                     tdu, p);
+  CUDA_TRY(pdl_launch(swiglu_bwd_dual_kernel, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), DU_SMEM, s, tdy, th2, twd, twgu, tact, tdg,
+                                                                                     tdu, p));
   return check_launch("swiglu_bwd_dual_kernel");
 }
 
 int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cudaStream_t s) {
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4096);
-  cast_f32_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(src, dst, n, e->prec);
+  CUDA_TRY(pdl_launch(cast_f32_kernel, dim3((unsigned)std::max<int64_t>(blocks, 1)), dim3(256), 0, s, src, dst, n, e->prec));
   return check_launch("cast_f32_kernel");
 }
 
@@ -522,7 +582,7 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
       set = true;
     }
     dim3 grid((unsigned)(tokens / a.T) * a.H, (unsigned)((a.T + 127) / 128));
-    attn_fwd_tc_kernel<<<grid, ATC_THREADS, ATC_SMEM, s>>>(tq, t);
+    CUDA_TRY(pdl_launch(attn_fwd_tc_kernel, dim3(grid), dim3(ATC_THREADS), ATC_SMEM, s, tq, t));
     return check_launch("attn_fwd_tc_kernel");
   }
   if (backward && e->prec == PREC_BF16 && hd == 64 && a.T % 128 == 0 && a.T <= 256) {
@@ -536,7 +596,7 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
       CUDA_TRY(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ABT_SMEM));
       set = true;
     }
-    attn_bwd_tc_kernel<<<(unsigned)((tokens / a.T) * a.H), ABT_THREADS, ABT_SMEM, s>>>(tq, tdo, t);
+    CUDA_TRY(pdl_launch(attn_bwd_tc_kernel, dim3((unsigned)((tokens / a.T) * a.H)), dim3(ABT_THREADS), ABT_SMEM, s, tq, tdo, t));
     return check_launch("attn_bwd_tc_kernel");
   }
   ProfScope prof(backward ? "attn_bwd" : "attn_fwd", (backward ? 4.0 : 2.0) * tokens * a.T * a.m,
@@ -551,14 +611,14 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
   case D: {                                                                                               \
     if (!backward) {                                                                                      \
       CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-      attn_fwd_kernel<D><<<grid, 256, sm, s>>>(a);                                                        \
+      CUDA_TRY(pdl_launch(attn_fwd_kernel<D>, dim3(grid), dim3(256), sm, s, a));                                                        \
       return check_launch("attn_fwd_kernel");                                                             \
     }                                                                                                     \
     CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    attn_bwd_dq_kernel<D><<<grid, 256, sm, s>>>(a);                                                       \
+    CUDA_TRY(pdl_launch(attn_bwd_dq_kernel<D>, dim3(grid), dim3(256), sm, s, a));                                                       \
     TRY(check_launch("attn_bwd_dq_kernel"));                                                              \
-    attn_bwd_dkv_kernel<D><<<grid, 256, sm, s>>>(a);                                                      \
+    CUDA_TRY(pdl_launch(attn_bwd_dkv_kernel<D>, dim3(grid), dim3(256), sm, s, a));                                                      \
     return check_launch("attn_bwd_dkv_kernel");                                                           \
   }
   switch (hd) {
@@ -1098,7 +1158,7 @@ int mecefo_embedding_forward(mecefo_engine* e, const int64_t* tokens, const floa
                              void* stream) {
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if (n <= 0) return MECEFO_OK;
-  embedding_fwd_kernel<<<(unsigned)n, 128, 0, s>>>(tokens, emb, x, (int)n, (int)e->d.hidden);
+  CUDA_TRY(pdl_launch(embedding_fwd_kernel, dim3((unsigned)n), dim3(128), 0, s, tokens, emb, x, (int)n, (int)e->d.hidden));
   return check_launch("embedding_fwd_kernel");
 }
 
@@ -1115,10 +1175,14 @@ int mecefo_head_logits(mecefo_engine* e, const float* x_last, const float* final
   return run_gemm(e, g, s);
 }
 
-int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens, float* loss,
-                         void* wsp, size_t ws_bytes, void* stream) {
+int mecefo_cross_entropy_grouped(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens,
+                                 int64_t group_rows, float* loss, void* wsp, size_t ws_bytes, void* stream) {
   auto s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t b = tokens, V = e->d.vocab;
+  if (group_rows <= 0 || tokens % group_rows != 0)
+    return set_err(MECEFO_ERR_CONTRACT, "%lld rows do not split into groups of %lld", (long long)tokens,
+                   (long long)group_rows);
+  const float inv_n = 1.f / (float)group_rows;
   Ws ws(wsp, ws_bytes);
   float* rows;
   int* bad;
@@ -1127,17 +1191,22 @@ int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets,
   CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
   ProfScope prof("cross_entropy", 0.0, 2.0 * b * V * e->ps, s);
   if (e->prec == PREC_BF16 && V % 8 == 0) {
-    cross_entropy_warp_kernel<<<(unsigned)((b + 7) / 8), 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(logits), V,
-                                                                       targets, rows, (int)b, (int)V, 1.f / (float)b,
-                                                                       bad);
+    CUDA_TRY(pdl_launch(cross_entropy_warp_kernel, dim3((unsigned)((b + 7) / 8)), dim3(256), 0, s,
+                        reinterpret_cast<__nv_bfloat16*>(logits), V, targets, rows, (int)b, (int)V, inv_n, bad));
     TRY(check_launch("cross_entropy_warp_kernel"));
   } else {
-    cross_entropy_kernel<<<(unsigned)b, 512, 0, s>>>(logits, V, targets, rows, (int)b, (int)V, 1.f / (float)b, e->prec,
-                                                      bad);
+    CUDA_TRY(pdl_launch(cross_entropy_kernel, dim3((unsigned)b), dim3(512), 0, s, logits, V, targets, rows, (int)b,
+                        (int)V, inv_n, e->prec, bad));
     TRY(check_launch("cross_entropy_kernel"));
   }
-  mean_kernel<<<1, 1024, 0, s>>>(rows, (int)b, loss);
+  CUDA_TRY(pdl_launch(mean_kernel, dim3((unsigned)(tokens / group_rows)), dim3(1024), 0, s, rows, (int)group_rows,
+                      loss));
   return check_launch("mean_kernel");
+}
+
+int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens, float* loss,
+                         void* wsp, size_t ws_bytes, void* stream) {
+  return mecefo_cross_entropy_grouped(e, logits, targets, tokens, tokens, loss, wsp, ws_bytes, stream);
 }
 
 int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
@@ -1176,14 +1245,14 @@ int mecefo_embedding_backward(mecefo_engine* e, const int64_t* tokens, const flo
                               int64_t n, void* stream) {
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if (n <= 0) return MECEFO_OK;
-  embedding_bwd_kernel<<<(unsigned)n, 128, 0, s>>>(tokens, dx0, g_emb, (int)n, (int)e->d.hidden, alpha);
+  CUDA_TRY(pdl_launch(embedding_bwd_kernel, dim3((unsigned)n), dim3(128), 0, s, tokens, dx0, g_emb, (int)n, (int)e->d.hidden, alpha));
   return check_launch("embedding_bwd_kernel");
 }
 
 int mecefo_scale_accumulate(const float* src, float* out, int64_t n, float alpha, float beta, void* stream) {
   if (n <= 0) return MECEFO_OK;
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8 * kNumSMs);
-  axpby_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(src, out, n, alpha, beta);
+  CUDA_TRY(pdl_launch(axpby_kernel, dim3((unsigned)blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), src, out, n, alpha, beta));
   return check_launch("axpby_kernel");
 }
 
@@ -1195,7 +1264,7 @@ int mecefo_cast(mecefo_engine* e, const float* src, void* dst, int64_t n, void* 
 int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream) {
   if (n <= 0) return MECEFO_OK;
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8 * kNumSMs);
-  nonfinite_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(v, n, flag);
+  CUDA_TRY(pdl_launch(nonfinite_kernel, dim3((unsigned)blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), v, n, flag));
   return check_launch("nonfinite_kernel");
 }
 
@@ -1208,9 +1277,9 @@ int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t
   auto s = reinterpret_cast<cudaStream_t>(stream);
   ProfScope prof("adamw", 0.0, 0.0, s);
   const unsigned grid = 8 * kNumSMs;  // grid-stride over the concatenated active segments
-  adamw_kernel<<<grid, 256, (nseg + 1) * sizeof(int64_t), s>>>(reinterpret_cast<const AdamSeg*>(segs), nseg, w, grad,
+  CUDA_TRY(pdl_launch(adamw_kernel, dim3(grid), dim3(256), (nseg + 1) * sizeof(int64_t), s, reinterpret_cast<const AdamSeg*>(segs), nseg, w, grad,
                                                                m1, m2, shadow, e ? e->prec : PREC_F32, beta1, beta2,
-                                                               eps);
+                                                               eps));
   return check_launch("adamw_kernel");
 }
 

@@ -60,6 +60,7 @@ struct GemmDev {
   int kb_per_split;      // k-blocks (of 64) per split
   int kblocks;           // total k-blocks
   int tiles_m, tiles_n, num_tiles;
+  int tiles_m_cl, num_tiles_cl;  // tiles in units of CTA clusters along M (CL = 1 or 2)
   Epilogue epi;
 };
 
@@ -221,6 +222,15 @@ __device__ __forceinline__ void decode_tile(const GemmDev& p, int t, int& mt, in
   nt = rest % p.tiles_n;
   ks = rest / p.tiles_n;
 }
+// Cluster tile t (pairs of M tiles sharing one B tile) -> this CTA's tile.
+__device__ __forceinline__ void decode_tile_cl(const GemmDev& p, int t, int crank, int cl, int& mt, int& nt,
+                                               int& ks) {
+  const int mp = t % p.tiles_m_cl;
+  int rest = t / p.tiles_m_cl;
+  nt = rest % p.tiles_n;
+  ks = rest / p.tiles_n;
+  mt = mp * cl + crank;
+}
 
 // ---------------------------------------------------------------------------
 // tcgen05 / TMA / mbarrier primitives (inline PTX, sm_100a)
@@ -257,6 +267,28 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -351,68 +383,82 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 // One warp writes its 32 rows x 32 columns to the staging buffer in the TMA
 // swizzle layout (fp32: 128-B rows, SWIZZLE_128B; bf16: 64-B rows,
 // SWIZZLE_64B) and lane 0 issues the bulk store / reduce-add.
-__device__ __forceinline__ void stage_and_store(uint8_t* stg, const CUtensorMap* map, const float* v, int prec,
-                                                int reduce, int c0, int r0, int lane) {
+// Epilogue staging, in 16-column halves of a 32-column chunk so the live
+// register set stays small (no spills at the 168-register cap of 384
+// threads). Layout = the TMA swizzle of the store map: fp32 -> 128-B rows,
+// SWIZZLE_128B; bf16 -> 64-B rows, SWIZZLE_64B.
+__device__ __forceinline__ void stage_wait(int lane) {
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   __syncwarp();
+}
+__device__ __forceinline__ void stage_write16(uint8_t* stg, const float* v, int prec, int half, int lane) {
   if (prec == PREC_F32) {
     uint8_t* row = stg + lane * 128;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int q = 0; q < 4; ++q) {
+      const int u = half * 4 + q;
       *reinterpret_cast<float4*>(row + ((u ^ (lane & 7)) << 4)) =
-          make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
   } else {
     uint8_t* row = stg + lane * 64;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int q = 0; q < 2; ++q) {
+      const int u = half * 2 + q;
       uint32_t w[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * u + 2 * j], v[8 * u + 2 * j + 1]);
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * j], v[8 * q + 2 * j + 1]);
         w[j] = *reinterpret_cast<uint32_t*>(&h);
       }
       *reinterpret_cast<uint4*>(row + ((u ^ ((lane >> 1) & 3)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+}
+__device__ __forceinline__ void stage_commit(uint8_t* stg, const CUtensorMap* map, int reduce, int c0, int r0,
+                                             int lane) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if (lane == 0) tma_store_2d(map, stg, c0, r0, reduce);
 }
 
-// Epilogue math for output slot `slot` on 32 consecutive output columns n0..
-// of row r (tcgen05 path): 0 = out / act, 1 = gate or d_gate, 2 = up or d_up.
-__device__ __forceinline__ void load32(const void* base, int64_t idx, float* v, int cnt, int prec) {
-  load16(base, idx, v, min(cnt, 16), prec);
-  if (cnt > 16) load16(base, idx + 16, v + 16, cnt - 16, prec);
+__device__ __forceinline__ void stage_store32(uint8_t* stg, const CUtensorMap* map, const float* v, int prec,
+                                              int reduce, int c0, int r0, int lane) {
+  stage_wait(lane);
+  stage_write16(stg, v, prec, 0, lane);
+  stage_write16(stg, v + 16, prec, 1, lane);
+  stage_commit(stg, map, reduce, c0, r0, lane);
 }
 
-__device__ __forceinline__ void epi_slot32(const Epilogue& e, int slot, int r, int n0, int cnt, bool row_ok,
+// Epilogue math for output slot `slot` on 16 consecutive output columns n0..
+// of row r (tcgen05 path): 0 = out / act, 1 = gate or d_gate, 2 = up or d_up.
+__device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, int n0, int cnt, bool row_ok,
                                            const float* g, const float* u, float* o) {
   if (e.kind == EPI_STORE || e.kind == EPI_ATOMIC) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) o[j] = g[j] * e.alpha;
+    for (int j = 0; j < 16; ++j) o[j] = g[j] * e.alpha;
     if (e.rope_cos && n0 < e.rope_cols && row_ok) {
       const int pos = r % e.rope_T, half = e.rope_hd >> 1;
-      if ((e.rope_hd & 31) == 0 && n0 + 32 <= e.rope_cols) {
-        // the 32-column chunk lies inside one head: 16 consecutive (cos, sin)
+      if ((e.rope_hd & 15) == 0 && n0 + 16 <= e.rope_cols) {
+        // the 16-column span lies inside one head: 8 consecutive (cos, sin)
         const int base = pos * half + ((n0 % e.rope_hd) >> 1);
-        float cs[16], sn[16];
+        float cs[8], sn[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const float4 c4 = __ldg(reinterpret_cast<const float4*>(e.rope_cos + base) + q);
           const float4 s4 = __ldg(reinterpret_cast<const float4*>(e.rope_sin + base) + q);
           cs[4 * q] = c4.x; cs[4 * q + 1] = c4.y; cs[4 * q + 2] = c4.z; cs[4 * q + 3] = c4.w;
           sn[4 * q] = s4.x; sn[4 * q + 1] = s4.y; sn[4 * q + 2] = s4.z; sn[4 * q + 3] = s4.w;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           const float ev = o[2 * j], od = o[2 * j + 1];
           o[2 * j] = ev * cs[j] - od * sn[j];
           o[2 * j + 1] = ev * sn[j] + od * cs[j];
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           const int c = n0 + 2 * j;
           if (c < e.rope_cols) {
             const int pi = pos * half + ((c % e.rope_hd) >> 1);
@@ -424,24 +470,24 @@ __device__ __forceinline__ void epi_slot32(const Epilogue& e, int slot, int r, i
         }
       }
     }
-    if (e.residual && row_ok) {
-      float t[32];
-      load32(e.residual, (int64_t)r * e.ldr + n0, t, cnt, PREC_F32);
+    if (e.residual && row_ok && cnt > 0) {
+      float t[16];
+      load16(e.residual, (int64_t)r * e.ldr + n0, t, min(cnt, 16), PREC_F32);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) o[j] += t[j];
+      for (int j = 0; j < 16; ++j) o[j] += t[j];
     }
     return;
   }
   if (e.kind == EPI_SWIGLU_BWD_CACHED) {  // g = d_act; aux = cached gate | up
-    float gt[32], up[32];
+    float gt[16], up[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) { gt[j] = 0.f; up[j] = 0.f; }
-    if (row_ok) {
-      load32(e.aux, (int64_t)r * e.ldaux + n0, gt, cnt, e.act_prec);
-      if (slot == 1) load32(e.aux, (int64_t)r * e.ldaux + e.offaux + n0, up, cnt, e.act_prec);
+    for (int j = 0; j < 16; ++j) { gt[j] = 0.f; up[j] = 0.f; }
+    if (row_ok && cnt > 0) {
+      load16(e.aux, (int64_t)r * e.ldaux + n0, gt, min(cnt, 16), e.act_prec);
+      if (slot == 1) load16(e.aux, (int64_t)r * e.ldaux + e.offaux + n0, up, min(cnt, 16), e.act_prec);
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
+    for (int j = 0; j < 16; ++j)
       o[j] = slot == 2 ? g[j] * silu_f(gt[j])                    // d_up   (model.py:252)
                        : (g[j] * up[j]) * silu_grad_f(gt[j]);    // d_gate (model.py:251,253)
     return;
@@ -449,24 +495,24 @@ __device__ __forceinline__ void epi_slot32(const Epilogue& e, int slot, int r, i
   // paired SwiGLU kinds: g = gate, u = up
   if (slot == 0) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) o[j] = silu_f(g[j]) * u[j];  // act (model.py:216)
+    for (int j = 0; j < 16; ++j) o[j] = silu_f(g[j]) * u[j];  // act (model.py:216)
     return;
   }
   if (e.kind == EPI_SWIGLU_FWD) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) o[j] = slot == 1 ? g[j] : u[j];
+    for (int j = 0; j < 16; ++j) o[j] = slot == 1 ? g[j] : u[j];
     return;
   }
-  float d[32];
+  float d[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) d[j] = 0.f;
-  if (row_ok) load32(e.aux, (int64_t)r * e.ldaux + n0, d, cnt, e.act_prec);
+  for (int j = 0; j < 16; ++j) d[j] = 0.f;
+  if (row_ok && cnt > 0) load16(e.aux, (int64_t)r * e.ldaux + n0, d, min(cnt, 16), e.act_prec);
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
+  for (int j = 0; j < 16; ++j)
     o[j] = slot == 2 ? d[j] * silu_f(g[j]) : (d[j] * u[j]) * silu_grad_f(g[j]);
 }
 
-template <int BN, bool A_KMAJOR, bool B_KMAJOR>
+template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
@@ -489,7 +535,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -499,6 +545,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int cl_id = blockIdx.x / CL, n_cl = gridDim.x / CL;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"((uint32_t)C::TMEM_COLS)
@@ -507,6 +556,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
+  griddep_wait();  // predecessor outputs are visible from here on
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -515,9 +566,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // ===== TMA producer =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
         int mt, nt, ks;
-        decode_tile(p, t, mt, nt, ks);
+        decode_tile_cl(p, t, crank, CL, mt, nt, ks);
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -533,7 +584,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_load_2d(a + 8192, &tmA, &full[stage], mt * TC_BM + 64, k0);
           }
           if (B_KMAJOR) {
-            if (!p.paired) {
+            if (CL > 1) {  // this CTA's half of the B tile, multicast to the pair
+              const int row = p.paired ? (crank == 0 ? nt * (BN / 2) : nt * (BN / 2) + (int)p.pair_off)
+                                       : nt * BN + crank * (BN / 2);
+              tma_load_2d_mc(b + crank * (BN / 2) * 128, &tmB, &full[stage], k0, row, kMask);
+            } else if (!p.paired) {
               tma_load_2d(b, &tmB, &full[stage], k0, nt * BN);
             } else {
               tma_load_2d(b, &tmB, &full[stage], k0, nt * (BN / 2));
@@ -543,12 +598,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             constexpr int NCH = BN / 64;
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
+              if (CL > 1 && c / (NCH / CL) != crank) continue;
               int col;
               if (!p.paired)
                 col = nt * BN + c * 64;
               else
                 col = (c < NCH / 2) ? nt * (BN / 2) + c * 64 : nt * (BN / 2) + (int)p.pair_off + (c - NCH / 2) * 64;
-              tma_load_2d(b + c * 8192, &tmB, &full[stage], col, k0);
+              if (CL > 1)
+                tma_load_2d_mc(b + c * 8192, &tmB, &full[stage], col, k0, kMask);
+              else
+                tma_load_2d(b + c * 8192, &tmB, &full[stage], col, k0);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -565,9 +624,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
         int mt, nt, ks;
-        decode_tile(p, t, mt, nt, ks);
+        decode_tile_cl(p, t, crank, CL, mt, nt, ks);
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -584,7 +643,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint64_t bd = B_KMAJOR ? make_sdesc(b_addr + k * 32, 16, 1024) : make_sdesc(b_addr + k * 2048, 8192, 1024);
             tc_mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
+          if (CL > 1)
+            tc_commit_mc(&empty[stage], kMask);  // the stage holds the peer's multicast half too
+          else
+            tc_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[acc]);
@@ -601,9 +663,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t acc_phase = 0;
     constexpr int NCHUNK_PLAIN = BN / 32;
     constexpr int NCHUNK_PAIR = BN / 64;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
       int mt, nt, ks;
-      decode_tile(p, t, mt, nt, ks);
+      decode_tile_cl(p, t, crank, CL, mt, nt, ks);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int r0 = mt * TC_BM + quad * 32;
@@ -613,32 +675,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
 #pragma unroll 1
       for (int c = half; c < nchunks; c += 2) {
-        float g[32], u[32];
-        int n0;
-        if (!p.paired) {
-          tmem_ld32(taddr + c * 32, g);
-          n0 = nt * BN + c * 32;
-        } else {
-          tmem_ld32(taddr + c * 32, g);
-          tmem_ld32(taddr + BN / 2 + c * 32, u);
-          n0 = nt * (BN / 2) + c * 32;
-        }
+        const int n0 = (p.paired ? nt * (BN / 2) : nt * BN) + c * 32;
         if (n0 >= p.N) continue;  // warp-uniform
-        const int cnt = min(32, p.N - n0);
-        if (outs.used[0]) {
-          float o[32];
-          epi_slot32(p.epi, 0, row, n0, cnt, row_ok, g, u, o);
-          stage_and_store(stg, &tmO0, o, outs.prec[0], outs.reduce[0], n0, r0, lane);
-        }
-        if (outs.used[1]) {
-          float o[32];
-          epi_slot32(p.epi, 1, row, n0, cnt, row_ok, g, u, o);
-          stage_and_store(stg, &tmO1, o, outs.prec[1], outs.reduce[1], n0, r0, lane);
-        }
-        if (outs.used[2]) {
-          float o[32];
-          epi_slot32(p.epi, 2, row, n0, cnt, row_ok, g, u, o);
-          stage_and_store(stg, &tmO2, o, outs.prec[2], outs.reduce[2], n0, r0, lane);
+#pragma unroll 1
+        for (int slot = 0; slot < 3; ++slot) {
+          if (!outs.used[slot]) continue;
+          stage_wait(lane);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float g[16], u[16], o[16];
+            tmem_ld16(taddr + c * 32 + hh * 16, g);
+            if (p.paired) tmem_ld16(taddr + BN / 2 + c * 32 + hh * 16, u);
+            const int n0h = n0 + hh * 16;
+            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g, u, o);
+            stage_write16(stg, o, outs.prec[slot], hh, lane);
+          }
+          stage_commit(stg, slot == 0 ? &tmO0 : (slot == 1 ? &tmO1 : &tmO2), outs.reduce[slot], n0, r0, lane);
         }
       }
       tc_fence_before();
@@ -650,6 +702,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)C::TMEM_COLS)
@@ -670,6 +723,7 @@ struct SimtOperand {
 };
 
 __global__ void __launch_bounds__(256) gemm_simt_kernel(SimtOperand A, SimtOperand B, GemmDev p) {
+  griddep_wait();
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   __shared__ float Cs[64][65];

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  griddep_wait();  // predecessor outputs are visible from here on
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -139,22 +140,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_arrive(&tempty[acc]);  // TMEM drained into registers: release it to the MMA early
       const int n0 = nt * DU_NP + half * 32;
       if (n0 < p.NP) {
-        // g <- sigmoid(gate), kept for all three outputs (one exp per element)
-        float sg[32];
+        // g <- sigmoid(gate) in place; u <- silu(gate)*... reuse registers to stay spill-free
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sg[j] = sigmoid_f(g[j]);
-        float o[32];
-        if (p.has_act) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = g[j] * sg[j] * u[j];                              // act
-          stage_and_store(stg, &tmAct, o, PREC_BF16, 0, n0, r0, lane);
+        for (int j = 0; j < 32; ++j) {
+          const float sg = sigmoid_f(g[j]);
+          const float act = g[j] * sg * u[j];
+          const float dg = (d[j] * u[j]) * (sg * (1.f + g[j] * (1.f - sg)));
+          const float du = d[j] * (g[j] * sg);
+          g[j] = dg;
+          u[j] = du;
+          d[j] = act;
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = (d[j] * u[j]) * (sg[j] * (1.f + g[j] * (1.f - sg[j])));  // d_gate
-        stage_and_store(stg, &tmDg, o, PREC_BF16, 0, n0, r0, lane);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = d[j] * (g[j] * sg[j]);                              // d_up
-        stage_and_store(stg, &tmDu, o, PREC_BF16, 0, n0, r0, lane);
+        if (p.has_act) stage_store32(stg, &tmAct, d, PREC_BF16, 0, n0, r0, lane);
+        stage_store32(stg, &tmDg, g, PREC_BF16, 0, n0, r0, lane);
+        stage_store32(stg, &tmDu, u, PREC_BF16, 0, n0, r0, lane);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }

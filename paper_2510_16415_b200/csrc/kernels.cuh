@@ -15,6 +15,7 @@ constexpr float kRmsEps = 1e-6f;  // model.py:27
 // ---------------------------------------------------------------------------
 __global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ g, void* __restrict__ out,
                                    float* __restrict__ inv_out, int rows, int m, int out_prec) {
+  griddep_wait();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -63,6 +64,7 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const float* __r
                                    const float* __restrict__ inv, const float* __restrict__ d,
                                    const float* __restrict__ resid, float* __restrict__ dx, void* __restrict__ dx_lp,
                                    int lp_prec, float* __restrict__ partial, int rows, int m, int rows_per_block) {
+  griddep_wait();
   extern __shared__ float sh[];  // [8][m] per-warp column partials
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* acc = sh + wid * m;
@@ -103,6 +105,7 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const float* __r
 // Block (32 x 8): 32 columns, 8 row-strided partial sums each, fixed order.
 __global__ void colsum_finalize_kernel(const float* __restrict__ partial, int nblocks, int m, float* __restrict__ out,
                                        float alpha, float beta) {
+  griddep_wait();
   __shared__ float red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
@@ -124,6 +127,7 @@ __global__ void colsum_finalize_kernel(const float* __restrict__ partial, int nb
 // ---------------------------------------------------------------------------
 __global__ void embedding_fwd_kernel(const int64_t* __restrict__ tok, const float* __restrict__ emb,
                                      float* __restrict__ out, int rows, int m) {
+  griddep_wait();
   const int row = blockIdx.x;
   if (row >= rows) return;
   const float* e = emb + tok[row] * (int64_t)m;
@@ -133,6 +137,7 @@ __global__ void embedding_fwd_kernel(const int64_t* __restrict__ tok, const floa
 
 __global__ void embedding_bwd_kernel(const int64_t* __restrict__ tok, const float* __restrict__ dx,
                                      float* __restrict__ grad, int rows, int m, float alpha) {
+  griddep_wait();
   const int row = blockIdx.x;
   if (row >= rows) return;
   float* gp = grad + tok[row] * (int64_t)m;
@@ -148,6 +153,7 @@ __global__ void embedding_bwd_kernel(const int64_t* __restrict__ tok, const floa
 __global__ void cross_entropy_kernel(void* __restrict__ logits, int64_t ld, const int64_t* __restrict__ targets,
                                      float* __restrict__ loss_rows, int rows, int V, float inv_n, int prec,
                                      int* __restrict__ bad_target) {
+  griddep_wait();
   __shared__ float red[32];
   const int row = blockIdx.x;
   if (row >= rows) return;
@@ -175,12 +181,15 @@ __global__ void cross_entropy_kernel(void* __restrict__ logits, int64_t ld, cons
 }
 
 // Deterministic mean of per-row losses into out[0] (single block).
+// One block per group of n consecutive values: out[g] = mean(v[g*n : (g+1)*n]).
 __global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  griddep_wait();
   __shared__ float red[32];
+  const float* vg = v + (int64_t)blockIdx.x * n;
   double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += vg[i];
   float t = block_sum((float)s, red);
-  if (threadIdx.x == 0) out[0] = t / (float)n;
+  if (threadIdx.x == 0) out[blockIdx.x] = t / (float)n;
 }
 
 // ---------------------------------------------------------------------------
@@ -188,16 +197,19 @@ __global__ void mean_kernel(const float* __restrict__ v, int n, float* __restric
 // ---------------------------------------------------------------------------
 __global__ void axpby_kernel(const float* __restrict__ src, float* __restrict__ out, int64_t n, float alpha,
                              float beta) {
+  griddep_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (beta != 0.f ? beta * out[i] : 0.f) + alpha * src[i];
 }
 
 __global__ void cast_f32_kernel(const float* __restrict__ src, void* __restrict__ dst, int64_t n, int prec) {
+  griddep_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     store_from_f32(dst, i, src[i], prec);
 }
 
 __global__ void nonfinite_kernel(const float* __restrict__ v, int64_t n, int* __restrict__ flag) {
+  griddep_wait();
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     bad |= !isfinite(v[i]);
@@ -226,6 +238,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(const AdamSeg* __restrict__ 
                                                     float* __restrict__ m1, float* __restrict__ m2,
                                                     void* __restrict__ shadow, int shadow_prec, float beta1,
                                                     float beta2, float eps) {
+  griddep_wait();
   extern __shared__ int64_t cum[];  // nseg + 1 prefix sums of numel
   if (threadIdx.x == 0) {
     int64_t c = 0;
@@ -320,6 +333,7 @@ template <int NV>
 __global__ void __launch_bounds__(256) rmsnorm_fwd_vec_kernel(const float* __restrict__ x, const float* __restrict__ g,
                                                               void* __restrict__ out, float* __restrict__ inv_out,
                                                               int rows, int m, int out_prec) {
+  griddep_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -358,6 +372,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_vec_kernel(const float* __res
                                                               void* __restrict__ dx_lp, int lp_prec,
                                                               float* __restrict__ partial, int rows, int m,
                                                               int rows_per_block) {
+  griddep_wait();
   extern __shared__ float4 red_dyn[];  // [8][NV * 32]
   float4 (*red)[NV * 32] = reinterpret_cast<float4 (*)[NV * 32]>(red_dyn);
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -433,6 +448,7 @@ __global__ void __launch_bounds__(256) cross_entropy_bf16_kernel(__nv_bfloat16* 
                                                                   const int64_t* __restrict__ targets,
                                                                   float* __restrict__ loss_rows, int rows, int V,
                                                                   float inv_n, int* __restrict__ bad_target) {
+  griddep_wait();
   __shared__ float red[32];
   __shared__ float zt_s;
   const int row = blockIdx.x;
@@ -504,6 +520,7 @@ __global__ void __launch_bounds__(256) cross_entropy_warp_kernel(__nv_bfloat16* 
                                                                   const int64_t* __restrict__ targets,
                                                                   float* __restrict__ loss_rows, int rows, int V,
                                                                   float inv_n, int* __restrict__ bad_target) {
+  griddep_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;

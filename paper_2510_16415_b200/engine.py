@@ -46,7 +46,7 @@ class StepEngine:
     def __init__(self, cfg: mdl.ModelConfig, precision: str = "bf16", seqs_per_microbatch: int = 32, r: int = 128,
                  tau: int = 100, optim_cfg: op.OptimConfig | None = None, seed: int = 0,
                  weights: mdl.ModelWeights | None = None, svd: SvdConfig | None = None, svd_budgeted: bool = False,
-                 group=None):
+                 group=None, fuse_lean: bool = True, max_group: int = 2):
         runtime.require_cuda()
         self.cfg = cfg
         self.precision = precision
@@ -65,7 +65,13 @@ class StepEngine:
         self.opt.ensure_flat(self.weights.total, self.device)
         self.grad = torch.zeros(self.weights.total, dtype=torch.float32, device=self.device)
         self.lws = [lw.struct() for lw in self.weights.layers]
-        b, m, L = self.b, cfg.hidden, cfg.layers
+        # Lean microbatches of one GPU can run as ONE pass over stacked rows
+        # (all row-wise / token-parallel kernels; per-rank losses kept apart):
+        # buffers are sized for `max_group` microbatches.
+        self.fuse_lean = fuse_lean
+        self.max_group = max(1, max_group)
+        self.iter = 0
+        b, m, L = self.b * self.max_group, cfg.hidden, cfg.layers
         f32 = dict(dtype=torch.float32, device=self.device)
         self.xs = [torch.empty(b, m, **f32) for _ in range(L + 1)]
         self.x1s = [torch.empty(b, m, **f32) for _ in range(L)]
@@ -78,6 +84,7 @@ class StepEngine:
         self.logits = torch.empty(b, cfg.vocab, dtype=self.dtype, device=self.device)
         self.tok = torch.empty(b, dtype=torch.int64, device=self.device)
         self.tgt = torch.empty(b, dtype=torch.int64, device=self.device)
+        self._loss_tmp = torch.zeros(self.max_group, dtype=torch.float32, device=self.device)
         self.rp = approx._pad16(r)
         nbytes = int(_lib.load().mecefo_workspace_bytes(self.eng.handle, b, self.rp))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -102,7 +109,7 @@ class StepEngine:
         if self.full is None:
             self.full = [None] * self.cfg.layers
         if self.full[l] is None:
-            self.full[l] = mdl._alloc_full_cache(self.cfg, self.b, self.dtype, self.device)
+            self.full[l] = mdl._alloc_full_cache(self.cfg, self.b, self.dtype, self.device)  # never fused
         return self.full[l]
 
     def proj(self, rank: int, layer: int) -> approx.ProjectionCache:
@@ -117,12 +124,59 @@ class StepEngine:
             self.projs[(rank, layer)].reset()
 
     # ---------------------------------------------------------- microbatch
+    def _fusable(self, mbs: list) -> bool:
+        """Several lean microbatches can share one pass iff every layer is lean
+        for all of them, their Eq. (1) weights agree and, per layer, their
+        projection bases are (or will be, after a common refresh) identical."""
+        if not self.fuse_lean or len(mbs) < 2 or len(mbs) > self.max_group:
+            return False
+        m0 = mbs[0]
+        for mb in mbs:
+            if not all(mb.lean) or any(a is not None for a in mb.alpha_mha):
+                return False
+            if mb.alpha_ffn != m0.alpha_ffn or mb.alpha_global != m0.alpha_global:
+                return False
+        for l in range(self.cfg.layers):
+            pcs = [self.proj(mb.rank, l) for mb in mbs]
+            due = [(not pc.basis) or pc.step % pc.refresh_period == 0 for pc in pcs]
+            if any(d != due[0] for d in due):
+                return False
+            if not due[0] and (pcs[0].token is None or any(pc.token != pcs[0].token for pc in pcs)):
+                return False
+        return True
+
+    def _projection(self, mbs: list, l: int):
+        """Refresh (if due) the basis of every rank in the group — computed once
+        and shared — and return the packed operands of the group's basis."""
+        pcs = [self.proj(mb.rank, l) for mb in mbs]
+        lead = pcs[0]
+        before = lead.refreshes
+        approx.refresh_projections(lead, self.weights.layers[l], self.svd, budgeted=self.svd_budgeted)
+        if lead.refreshes != before:
+            lead.token = ("svd", self.iter, l, self.r, self.svd)
+            for pc in pcs[1:]:  # same weights, same SvdConfig -> same basis
+                for k, v in lead.basis.items():
+                    pc.set_basis(k, v)
+                pc.token = lead.token
+                pc.refreshes += 1
+                pc.svd_calls += len(lead.basis)
+        return lead.packed(self.precision)
+
     def microbatch(self, mb: Microbatch, loss_ptr: int) -> None:
-        cfg, eng, b, s = self.cfg, self.eng, self.b, runtime.stream_ptr()
+        self._run([mb], loss_ptr)
+
+    def _run(self, mbs: list, loss_ptr: int) -> None:
+        """Forward + backward of len(mbs) microbatches stacked into one pass;
+        loss_ptr receives len(mbs) consecutive per-microbatch mean losses."""
+        cfg, eng, s = self.cfg, self.eng, runtime.stream_ptr()
+        n, b1 = len(mbs), self.b
+        b = n * b1
+        mb = mbs[0]
         w = self.weights
         ws, wn = self.ws.data_ptr(), self.ws.numel()
-        self.tok.copy_(mb.tokens.reshape(-1), non_blocking=True)
-        self.tgt.copy_(mb.targets.reshape(-1), non_blocking=True)
+        for i, m_ in enumerate(mbs):
+            self.tok[i * b1:(i + 1) * b1].copy_(m_.tokens.reshape(-1), non_blocking=True)
+            self.tgt[i * b1:(i + 1) * b1].copy_(m_.targets.reshape(-1), non_blocking=True)
         _lib.call("mecefo_embedding_forward", eng.handle, self.tok.data_ptr(),
                   w.master.data_ptr() + 4 * w.offsets["embedding"], self.xs[0].data_ptr(), b, s)
         caches = []
@@ -138,8 +192,8 @@ class StepEngine:
         _lib.call("mecefo_head_logits", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
                   w.shadow_view("unembedding").data_ptr(), b, self.xf.data_ptr(), self.inv_f.data_ptr(),
                   self.logits.data_ptr(), s)
-        _lib.call("mecefo_cross_entropy", eng.handle, self.logits.data_ptr(), self.tgt.data_ptr(), b, loss_ptr, ws, wn,
-                  s)
+        _lib.call("mecefo_cross_entropy_grouped", eng.handle, self.logits.data_ptr(), self.tgt.data_ptr(), b, b1,
+                  loss_ptr, ws, wn, s)
         cur = 0
         _lib.call("mecefo_head_backward", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
                   self.inv_f.data_ptr(), self.xf.data_ptr(), self.logits.data_ptr(),
@@ -149,15 +203,14 @@ class StepEngine:
             nxt = 1 - cur
             g = self._layer_grads(l, mb.alpha_mha[l], mb.alpha_ffn)
             if mb.lean[l]:
-                pc = self.proj(mb.rank, l)
-                approx.refresh_projections(pc, w.layers[l], self.svd, budgeted=self.svd_budgeted)
-                pst, keep, rp = pc.packed(self.precision)
+                pst, keep, rp = self._projection(mbs, l)
                 self._keep = keep
                 _lib.call("mecefo_backward_block_neighbor", eng.handle, ctypes.byref(self.lws[l]),
                           ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
                           self.dx[nxt].data_ptr(), runtime.ptr(self.dx_c[nxt]), ctypes.byref(g), ctypes.byref(pst), b,
                           ws, wn, s)
-                pc.step += 1
+                for m_ in mbs:
+                    self.proj(m_.rank, l).step += 1
             else:
                 _lib.call("mecefo_backward_block_exact", eng.handle, ctypes.byref(self.lws[l]),
                           ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
@@ -204,8 +257,18 @@ class StepEngine:
     def _body(self, mbs: list, losses: torch.Tensor) -> None:
         self.grad.zero_()
         losses.zero_()
-        for mb in mbs:
-            self.microbatch(mb, losses.data_ptr() + 4 * mb.rank)
+        if self._fusable(mbs):
+            ranks = [mb.rank for mb in mbs]
+            if ranks == list(range(ranks[0], ranks[0] + len(ranks))):
+                self._run(mbs, losses.data_ptr() + 4 * ranks[0])  # per-rank losses land in place
+            else:
+                self._run(mbs, self._loss_tmp.data_ptr())
+                for i, j in enumerate(ranks):  # device-to-device, graph-capturable
+                    losses[j:j + 1].copy_(self._loss_tmp[i:i + 1])
+        else:
+            for mb in mbs:
+                self.microbatch(mb, losses.data_ptr() + 4 * mb.rank)
+        self.iter += 1
         if self.group is not None:
             import torch.distributed as dist
 
@@ -248,6 +311,7 @@ class StepEngine:
             self.graphs.append(g)
         for k, v in steps.items():  # capture ran the host bookkeeping once; undo it
             self.projs[k].step = v
+        self.iter -= 2
         torch.cuda.synchronize()
 
     def replay(self, lr: float) -> torch.Tensor:
@@ -265,6 +329,7 @@ class StepEngine:
             for l in range(self.cfg.layers):
                 if mb.lean[l]:
                     self.proj(mb.rank, l).step += 1
+        self.iter += 1
         self.graphs[slot].replay()
         ev.record()
         return self.losses

@@ -133,3 +133,40 @@ def test_graph_replay_matches_eager(cuda):
     assert s0 == s1 and p0 == p1
     assert torch.allclose(l0, l1, rtol=1e-3, atol=1e-4)
     assert R.rel_err(w0.cpu().numpy(), w1.cpu().numpy()) < 1e-3
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("bf16", 5e-2)])
+def test_fused_lean_microbatches_match_reference(cuda, prec, tol):
+    """The doubled GPU's two lean microbatches run as ONE stacked pass when
+    their ranks share projection bases; Eq. (1) gradients and per-rank losses
+    are those of the reference's separate rank passes."""
+    batches = _batches(2, 2, seed=7)
+    eng, bases = _engine(prec, 2)
+    for l in range(2):  # rank 1 adopts rank 0's bases (same provenance token)
+        for k, v in bases[(0, l)].items():
+            eng.proj(1, l).set_basis(k, v)
+        eng.proj(1, l).token = eng.proj(0, l).token
+        bases[(1, l)] = bases[(0, l)]
+    mbs, lean, skip = _plan(2, {1}, batches)
+    assert eng._fusable(mbs)
+    losses = torch.zeros(2, device="cuda")
+    eng._body(mbs, losses)
+    torch.cuda.synchronize()
+    W = R.init_params(D0, 0)
+    per_rank, ref_losses = [], []
+    for j in range(2):
+        loss, g = R.rank_pass(D0, W, batches[j][0], batches[j][1], ["ffn_input_only"] * 2,
+                              {l: bases[(j, l)] for l in range(2)})
+        per_rank.append(g)
+        ref_losses.append(loss)
+    active = {(l, k): ([] if k in cluster_ref.MHA else [0, 1]) for l in range(2)
+              for k in cluster_ref.MHA + cluster_ref.FFN}
+    avg, skipped = cluster_ref.aggregate(per_rank, active, 2)
+    assert np.allclose(losses.cpu().numpy(), ref_losses, rtol=tol, atol=tol)
+    for name, shape, off in eng.weights.layout:
+        got = eng.grad[off: off + int(np.prod(shape))].view(shape).cpu().numpy()
+        if name in skipped:
+            assert not got.any(), name
+        else:
+            assert R.rel_err(got, avg[name]) < tol, name
+    assert all(eng.proj(j, l).step == 2 for j in range(2) for l in range(2))
