@@ -114,6 +114,11 @@ typedef struct {
   int32_t rank_pad;
   const void* v1[3];
   const void* v1t[3];
+  /* optional: gate and up bases packed side by side, v1_gu = [V1_gate | V1_up]
+   * (in, 2 rank_pad), and v1t_gu = [V1_gate^T ; V1_up^T] (2 rank_pad, in).
+   * When set, the gate/up low-rank Wgrads run as one merged chain. */
+  const void* v1_gu;
+  const void* v1t_gu;
 } mecefo_projection;
 
 /* AdamW segment: one named parameter of the flat buffer (optim.py:75-93). */

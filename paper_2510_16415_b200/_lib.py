@@ -90,6 +90,8 @@ class Projection(ctypes.Structure):
         ("rank_pad", c_int32),
         ("v1", c_void_p * 3),
         ("v1t", c_void_p * 3),
+        ("v1_gu", c_void_p),
+        ("v1t_gu", c_void_p),
     ]
 
 

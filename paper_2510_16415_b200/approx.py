@@ -89,10 +89,13 @@ class ProjectionCache:
             # refresh in place: packed engine operands keep their addresses
             # (captured CUDA graphs read them by pointer)
             for (prec, rp), (_, keep) in self._packed.items():
-                v, vt = keep[1 + 2 * FFN_KINDS.index(kind)], keep[2 + 2 * FFN_KINDS.index(kind)]
+                i = FFN_KINDS.index(kind)
+                v, vt = keep[2 + 2 * i], keep[3 + 2 * i]
                 v.zero_()
                 v[:, :t.shape[1]] = t.to(v.dtype)
                 vt.copy_(v.t())
+                if kind in ("gate", "up") and keep[1] is not None:
+                    keep[1][:, i * rp:(i + 1) * rp].copy_(v)
             return
         self._packed.clear()
 
@@ -119,10 +122,14 @@ class ProjectionCache:
                 else:
                     vt = v.t().contiguous()
                 tensors[k] = (v, vt)
-            keep = [vt_gu] + [t for k in FFN_KINDS for t in tensors[k]]
+            packed_gu = self.basis["up"].shape[0] == n_gu
+            # [V1_gate | V1_up] side by side for the merged up-projection
+            v1_gu = torch.cat([tensors["gate"][0], tensors["up"][0]], dim=1).contiguous() if packed_gu else None
+            keep = [vt_gu, v1_gu] + [t for k in FFN_KINDS for t in tensors[k]]
             st = _lib.Projection((ctypes.c_int32 * 3)(*ranks), rp,
                                  (ctypes.c_void_p * 3)(*[tensors[k][0].data_ptr() for k in FFN_KINDS]),
-                                 (ctypes.c_void_p * 3)(*[tensors[k][1].data_ptr() for k in FFN_KINDS]))
+                                 (ctypes.c_void_p * 3)(*[tensors[k][1].data_ptr() for k in FFN_KINDS]),
+                                 v1_gu.data_ptr() if packed_gu else None, vt_gu.data_ptr() if packed_gu else None)
             self._packed[key] = (st, keep)
         st, keep = self._packed[key]
         return st, keep, rp

@@ -743,8 +743,8 @@ size_t mecefo_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t ra
   const int64_t m = e->d.hidden, f = e->d.ffn, H = e->d.heads, ps = e->ps;
   const int64_t rp = std::max<int32_t>(rank_pad, 16);
   const int64_t per_tok = (6 * m + 4 * f + 3 * rp) * ps + 16 * m + 8 * H + 64;
-  const int64_t fixed = 3 * std::max(m, f) * rp * (4 + ps) + ((tokens + 63) / 64 + 8) * m * 4 * 2 +
-                        e->d.vocab * 4 + (4 << 20);
+  const int64_t fixed = 3 * std::max(m, f) * rp * (4 + ps) + 4 * f * rp * (4 + ps) + tokens * 2 * rp * ps +
+                        ((tokens + 63) / 64 + 8) * m * 4 * 2 + e->d.vocab * 4 + (4 << 20);
   return (size_t)(tokens * per_tok + fixed);
 }
 
@@ -842,6 +842,47 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
   for (int k = 0; k < 3; ++k)
     if (kinds[k].grad && (!pj->v1[k] || !pj->v1t[k]))
       return set_err(MECEFO_ERR_CONTRACT, "projection basis %d missing", k);
+  // Fully merged gate/up chain (packed bases supplied):
+  //   [P_g | P_u]  = h2 [V1_g | V1_u]                         (b, 2rp)
+  //   Q            = [d_gate | d_up]^T [P_g | P_u]             (2f, 2rp), split-K
+  //   [G_g ; G_u] += alpha blockdiag(Q) [V1_g | V1_u]^T        (2f, m) = the gate|up grad
+  if (kinds[0].grad && kinds[1].grad && pj->v1_gu && pj->v1t_gu && e->prec == PREC_BF16) {
+    float* Q2;
+    void* Q2c;
+    TRY(ws.take(2 * f * 2 * rp * 4, reinterpret_cast<void**>(&Q2)));
+    TRY(ws.take(2 * f * 2 * rp * ps, &Q2c));
+    GemmCall g;
+    g.M = b; g.N = 2 * rp; g.K = m;
+    g.a = {h2, m, true}; g.b = {pj->v1t_gu, m, true};
+    g.epi = epi_store(P, 2 * rp, e->prec);
+    g.tag = "lowrank.P";
+    TRY(run_gemm(e, g, s));
+    CUDA_TRY(cudaMemsetAsync(Q2, 0, 2 * f * 2 * rp * 4, s));
+    g = GemmCall();
+    g.M = 2 * f; g.N = 2 * rp; g.K = b;
+    g.a = {dcat, 2 * f, false}; g.b = {P, 2 * rp, false};
+    g.tag = "lowrank.Q";
+    TRY(gemm_accumulate(e, g, Q2, 2 * rp, 1.f, s));
+    {
+      const int64_t n = 4 * f * rp;
+      ProfScope prof("lowrank.cast", 0.0, 6.0 * n, s);
+      CUDA_TRY(pdl_launch(cast_blockdiag_kernel, dim3((unsigned)std::min<int64_t>((n + 255) / 256, 4 * kNumSMs)),
+                          dim3(256), 0, s, (const float*)Q2, Q2c, (int)f, (int)rp, e->prec));
+      TRY(check_launch("cast_blockdiag_kernel"));
+    }
+    g = GemmCall();
+    g.M = 2 * f; g.N = m; g.K = 2 * rp;
+    g.a = {Q2c, 2 * rp, true}; g.b = {pj->v1_gu, 2 * rp, true};
+    g.epi = epi_store(gr->gu, m, PREC_F32, gr->alpha_ffn, 1.f);
+    g.tag = "lowrank.up_proj";
+    TRY(run_gemm(e, g, s));
+    if (!kinds[2].grad) return MECEFO_OK;
+    mecefo_projection down_only = *pj;
+    mecefo_layer_grads gdown = *gr;
+    gdown.gu = nullptr;
+    down_only.v1_gu = down_only.v1t_gu = nullptr;
+    return lowrank_ffn_wgrads(e, ws, &down_only, dy_c, h2, act, dcat, &gdown, b, s);
+  }
   // gate and up share inp2 = h2: when their V1^T are stacked contiguously,
   // one GEMM produces [P_gate | P_up] (b, 2 rp).
   const bool merged = kinds[0].grad && kinds[1].grad &&

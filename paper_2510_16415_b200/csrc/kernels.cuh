@@ -208,6 +208,19 @@ __global__ void cast_f32_kernel(const float* __restrict__ src, void* __restrict_
     store_from_f32(dst, i, src[i], prec);
 }
 
+// Q (2f x 2r) fp32 -> compute precision, keeping only the diagonal blocks
+// [0,f)x[0,r) and [f,2f)x[r,2r) (the gate-gate and up-up products).
+__global__ void cast_blockdiag_kernel(const float* __restrict__ src, void* __restrict__ dst, int rows_half,
+                                      int cols_half, int prec) {
+  griddep_wait();
+  const int64_t n = (int64_t)4 * rows_half * cols_half;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (2 * cols_half), c = i % (2 * cols_half);
+    const bool keep = (r < rows_half) == (c < cols_half);
+    store_from_f32(dst, i, keep ? src[i] : 0.f, prec);
+  }
+}
+
 __global__ void nonfinite_kernel(const float* __restrict__ v, int64_t n, int* __restrict__ flag) {
   griddep_wait();
   bool bad = false;
