@@ -142,7 +142,7 @@ class ClockSampler:
                         self.samples.append(parts)
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.05)
 
         self._th = threading.Thread(target=run, daemon=True)
         self._th.start()
@@ -187,7 +187,7 @@ def _profile_records(lib):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
@@ -341,19 +341,25 @@ def main():
         kernels.append({"tag": tag, "ms_total": round(tms, 3), "launches": cnt, "share": round(tms / ms_prof, 4),
                         "tflops": round(fl / (tms / 1e3) / 1e12, 1) if fl else None,
                         "gbs": round(by / (tms / 1e3) / 1e9, 1)})
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            ncu_traffic = json.load(f)
+    except Exception:
+        ncu_traffic = {}
     if top:
         tag, (tms, cnt, fl, by) = top[0]
         avg_s = tms / cnt / 1e3
         if fl > 0:
             ach = fl / cnt / avg_s / 1e12
             roofline = {"kernel": tag, "bound": "tensor", "achieved": round(ach, 1), "peak": bf16_sus,
-                        "unit": "TFLOP/s", "frac": round(ach / bf16_sus, 4), "traffic": None,
+                        "unit": "TFLOP/s", "frac": round(ach / bf16_sus, 4),
+                        "traffic": ncu_traffic.get(tag, {}).get("bytes"),
                         "per_launch": f"{fl / cnt / 1e9:.3f} GFLOP algorithmic (2*M*N*K)",
                         "peak_source": f"{peak_src} bf16 sustained", "share_of_step": round(tms / ms_prof, 4)}
         else:
             ach = by / cnt / avg_s / 1e9
             roofline = {"kernel": tag, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                        "frac": round(ach / hbm, 4), "traffic": None,
+                        "frac": round(ach / hbm, 4), "traffic": ncu_traffic.get(tag, {}).get("bytes"),
                         "per_launch": f"{by / cnt / 1e6:.2f} MB algorithmic", "peak_source": peak_src,
                         "share_of_step": round(tms / ms_prof, 4)}
 
