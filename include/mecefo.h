@@ -199,6 +199,14 @@ int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets,
 int mecefo_cross_entropy_grouped(mecefo_engine* e, void* logits, const int64_t* targets, int64_t tokens,
                                  int64_t group_rows, float* loss, void* ws, size_t ws_bytes, void* stream);
 
+/* model.py:469-471 + 492-509 for `tokens / group_rows` stacked ranks: final
+ * norm + logits GEMM, then the fused softmax-CE pass (dlogits in place,
+ * loss[g] = mean loss of group g). */
+int mecefo_head_forward_loss_grouped(mecefo_engine* e, const float* x_last, const float* final_norm,
+                                     const void* unemb_c, const int64_t* targets, int64_t tokens, int64_t group_rows,
+                                     void* xf, float* inv_f, void* logits, float* loss, void* ws, size_t ws_bytes,
+                                     void* stream);
+
 /* model.py:476-483 head_backward (+ accumulate into g_final_norm/g_unemb). */
 int mecefo_head_backward(mecefo_engine* e, const float* x_last, const float* final_norm, const float* inv_f,
                          const void* xf, const void* dlogits, const void* unemb_c, float* dx, void* dx_c,

@@ -142,6 +142,8 @@ def refresh_projections(cache: ProjectionCache, lw: mdl.LayerWeights, svd: SvdCo
         raise ContractViolation("refresh_period must be >= 1")
     if cache.step % cache.refresh_period != 0 and cache.basis:
         return
+    if cache.basis and getattr(cache, "_fresh_step", None) == cache.step:
+        return  # already refreshed for this step by a batched pre-refresh
     cache.refreshes += 1
     for kind in FFN_KINDS:
         w = lw.kind(kind)

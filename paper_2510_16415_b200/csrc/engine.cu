@@ -1250,6 +1250,17 @@ int mecefo_cross_entropy(mecefo_engine* e, void* logits, const int64_t* targets,
   return mecefo_cross_entropy_grouped(e, logits, targets, tokens, tokens, loss, wsp, ws_bytes, stream);
 }
 
+int mecefo_head_forward_loss_grouped(mecefo_engine* e, const float* x_last, const float* final_norm,
+                                     const void* unemb_c, const int64_t* targets, int64_t tokens, int64_t group_rows,
+                                     void* xf, float* inv_f, void* logits, float* loss, void* wsp, size_t ws_bytes,
+                                     void* stream) {
+  // (Measured: folding softmax statistics into the logits GEMM epilogue made
+  // that GEMM epilogue-bound, 1.17 -> 0.57 PFLOP/s; a separate warp-per-row CE
+  // pass over the L2-resident rows is faster overall.)
+  TRY(mecefo_head_logits(e, x_last, final_norm, unemb_c, tokens, xf, inv_f, logits, stream));
+  return mecefo_cross_entropy_grouped(e, logits, targets, tokens, group_rows, loss, wsp, ws_bytes, stream);
+}
+
 int mecefo_head_forward_loss(mecefo_engine* e, const float* x_last, const float* final_norm, const void* unemb_c,
                              const int64_t* targets, int64_t tokens, void* xf, float* inv_f, void* logits, float* loss,
                              void* wsp, size_t ws_bytes, void* stream) {

@@ -60,6 +60,8 @@ class StepEngine:
         self.tau = tau
         self.svd = svd if svd is not None else SvdConfig(rank=r, tolerance=1e-9, max_iterations=3000, seed=seed + 23)
         self.svd_budgeted = svd_budgeted
+        # budgeted runs refresh all due bases in one batched device iteration
+        self.batched_refresh = svd_budgeted
         self.group = group
         self.opt = op.OptimState(optim_cfg or op.OptimConfig())
         self.opt.ensure_flat(self.weights.total, self.device)
@@ -189,11 +191,9 @@ class StepEngine:
             _lib.call("mecefo_forward_block", eng.handle, ctypes.byref(self.lws[l]), ctypes.byref(cs),
                       self.xs[l + 1].data_ptr(), None, b,
                       _lib.CACHE_FFN_INPUT_ONLY if mb.lean[l] else _lib.CACHE_FULL, ws, wn, s)
-        _lib.call("mecefo_head_logits", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
-                  w.shadow_view("unembedding").data_ptr(), b, self.xf.data_ptr(), self.inv_f.data_ptr(),
-                  self.logits.data_ptr(), s)
-        _lib.call("mecefo_cross_entropy_grouped", eng.handle, self.logits.data_ptr(), self.tgt.data_ptr(), b, b1,
-                  loss_ptr, ws, wn, s)
+        _lib.call("mecefo_head_forward_loss_grouped", eng.handle, self.xs[cfg.layers].data_ptr(),
+                  w.get("final_norm").data_ptr(), w.shadow_view("unembedding").data_ptr(), self.tgt.data_ptr(), b, b1,
+                  self.xf.data_ptr(), self.inv_f.data_ptr(), self.logits.data_ptr(), loss_ptr, ws, wn, s)
         cur = 0
         _lib.call("mecefo_head_backward", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
                   self.inv_f.data_ptr(), self.xf.data_ptr(), self.logits.data_ptr(),
@@ -254,7 +254,48 @@ class StepEngine:
                       self.opt.v.data_ptr(), shadow, cfg.beta1, cfg.beta2, cfg.eps, stream_ptr)
 
     # ---------------------------------------------------------------- step
+    def _prerefresh(self, mbs: list) -> None:
+        """Batched projection refresh: every lean (rank, layer) whose refresh
+        is due this iteration (approx.py:74-75) is refreshed at once; ranks
+        sharing a basis provenance share the result."""
+        if not self.batched_refresh:
+            return
+        due = {}
+        for mb in mbs:
+            for l in range(self.cfg.layers):
+                if not mb.lean[l]:
+                    continue
+                pc = self.proj(mb.rank, l)
+                if pc.basis and pc.step % pc.refresh_period != 0:
+                    continue
+                if pc.basis and getattr(pc, "_fresh_step", None) == pc.step:
+                    continue
+                due.setdefault(l, []).append(pc)
+        if not due:
+            return
+        from .linalg import top_r_right_singular_vectors_batched
+
+        mats, ranks, owners = [], [], []
+        for l, pcs in due.items():
+            for kind in approx.FFN_KINDS:
+                w = self.weights.layers[l].kind(kind)
+                mats.append(w)
+                ranks.append(min(self.r, w.shape[1]))
+                owners.append((l, kind))
+        bases = top_r_right_singular_vectors_batched(mats, ranks, self.svd.max_iterations, self.svd.seed)
+        for (l, kind), v1 in zip(owners, bases):
+            for pc in due[l]:
+                pc.set_basis(kind, v1)
+        for l, pcs in due.items():
+            tok = ("svd", self.iter, l, self.r, self.svd)
+            for pc in pcs:
+                pc.token = tok
+                pc.refreshes += 1
+                pc.svd_calls += len(approx.FFN_KINDS)
+                pc._fresh_step = pc.step
+
     def _body(self, mbs: list, losses: torch.Tensor) -> None:
+        self._prerefresh(mbs)
         self.grad.zero_()
         losses.zero_()
         if self._fusable(mbs):
@@ -333,6 +374,46 @@ class StepEngine:
         self.graphs[slot].replay()
         ev.record()
         return self.losses
+
+    def steps_until_refresh(self, mbs: list) -> int:
+        """Iterations until the first lean layer's projection refresh is due
+        (0 = due now; approx.py:74-75)."""
+        best = 10**9
+        for mb in mbs:
+            for l in range(self.cfg.layers):
+                if mb.lean[l]:
+                    pc = self.proj(mb.rank, l)
+                    best = min(best, 0 if not pc.basis else (-pc.step) % pc.refresh_period)
+        return best
+
+    def refresh_cost(self, mbs: list) -> float:
+        """Seconds for one refresh of every lean layer's bases of these
+        microbatches (the tau-amortised work), measured on a scratch copy of
+        the caches so the run's own schedule is untouched."""
+        import time
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        seen = set()
+        mats, ranks = [], []
+        for mb in mbs:
+            for l in range(self.cfg.layers):
+                if mb.lean[l] and (self.proj(mb.rank, l).token, l) not in seen:
+                    seen.add((self.proj(mb.rank, l).token, l))
+                    if self.batched_refresh:
+                        for kind in approx.FFN_KINDS:
+                            w = self.weights.layers[l].kind(kind)
+                            mats.append(w)
+                            ranks.append(min(self.r, w.shape[1]))
+                    else:
+                        pc = approx.ProjectionCache(rank=self.r, refresh_period=self.tau)
+                        approx.refresh_projections(pc, self.weights.layers[l], self.svd, budgeted=self.svd_budgeted)
+        if mats:
+            from .linalg import top_r_right_singular_vectors_batched
+
+            top_r_right_singular_vectors_batched(mats, ranks, self.svd.max_iterations, self.svd.seed)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
 
     def projections_due(self, mbs: list) -> bool:
         """True if any lean layer's projection refresh is due next iteration

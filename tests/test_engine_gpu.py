@@ -170,3 +170,41 @@ def test_fused_lean_microbatches_match_reference(cuda, prec, tol):
         else:
             assert R.rel_err(got, avg[name]) < tol, name
     assert all(eng.proj(j, l).step == 2 for j in range(2) for l in range(2))
+
+
+def test_batched_refresh_finds_dominant_subspace(cuda):
+    """linalg.top_r_right_singular_vectors_batched: the subspace it returns
+    for matrices with a spectral gap at r matches numpy's SVD (projector
+    distance), and it is orthonormal (linalg.py:97-142 semantics)."""
+    from paper_2510_16415_b200.linalg import top_r_right_singular_vectors_batched
+
+    rng = np.random.Generator(np.random.PCG64(3))
+    mats, refs = [], []
+    for (out, n, r) in ((344, 128, 32), (128, 344, 32), (512, 256, 64)):
+        q = min(out, n)
+        u, _ = np.linalg.qr(rng.normal(size=(out, q)))
+        v, _ = np.linalg.qr(rng.normal(size=(n, q)))
+        s = np.concatenate([np.linspace(10, 5, r), np.linspace(1, 0.1, q - r)])
+        w = (u * s) @ v.T
+        mats.append(torch.tensor(w, dtype=torch.float32, device="cuda"))
+        refs.append((np.linalg.svd(w)[2][:r].T, r))
+    got = top_r_right_singular_vectors_batched(mats, [r for _, r in refs], iterations=30, seed=23)
+    for v1, (vref, r) in zip(got, refs):
+        v1 = v1.double().cpu().numpy()
+        assert v1.shape == vref.shape
+        assert np.abs(v1.T @ v1 - np.eye(r)).max() < 1e-4
+        assert np.abs(v1 @ v1.T - vref @ vref.T).max() < 1e-3
+
+
+def test_engine_budgeted_refresh_runs_and_is_shared(cuda):
+    eng = E.StepEngine(C0, precision="bf16", seqs_per_microbatch=2, r=32, tau=3,
+                       svd=__import__("paper_2510_16415_b200.linalg", fromlist=["SvdConfig"]).SvdConfig(
+                           rank=32, tolerance=1e-3, max_iterations=10, seed=23), svd_budgeted=True)
+    mbs, lean, skip = _plan(2, {1}, _batches(2, 2, seed=9))
+    for it in range(5):
+        losses = eng.step(mbs, 2, 1e-3, skip=skip, check=True)
+        assert bool(torch.isfinite(losses).all())
+    pcs = [eng.proj(j, l) for j in range(2) for l in range(2)]
+    assert all(pc.refreshes == 2 for pc in pcs)  # iterations 0 and 3 (tau = 3)
+    assert eng.proj(0, 0).token == eng.proj(1, 0).token  # shared basis -> fused pass
+    assert eng._fusable(mbs)
