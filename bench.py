@@ -335,14 +335,17 @@ def main():
     with ClockSampler(local) as clk:
         ms, launches, wall = timed(degraded, skip_d, args.steps, graph=use_graph)
     tokens_per_step = R * b
-    value = tokens_per_step * args.steps / (ms / 1000.0)
-    # the tau-amortised projection refresh of this GPU's lean layers
-    t_refresh = eng.refresh_cost(degraded) if degraded else 0.0
+    value_steady = tokens_per_step * args.steps / (ms / 1000.0)
+    # the projection refresh of this GPU's lean layers, due once per tau steps:
+    # timed separately (median of 3, device-synchronised) and amortised into
+    # `value` — the timed legs themselves never contain a refresh
+    t_refresh = float(np.median([eng.refresh_cost(degraded) for _ in range(3)])) if degraded else 0.0
     if group is not None:
         tr = torch.tensor([t_refresh], device="cuda")
         dist.all_reduce(tr, op=dist.ReduceOp.MAX)
         t_refresh = float(tr.item())
-    value_amortized = tokens_per_step / ((ms / args.steps) / 1000.0 + t_refresh / eng.tau)
+    refresh_s_per_step = t_refresh / eng.tau
+    value = tokens_per_step / ((ms / args.steps) / 1000.0 + refresh_s_per_step)
     # per-kernel attribution: the same degraded iteration, eager, with CUDA
     # events around every kernel group (own timed region of K steps)
     ms_prof, _, _ = timed(degraded, skip_d, args.steps, profile=True)
@@ -402,7 +405,7 @@ def main():
     else:
         eng.step(degraded_e2e, R, lr, skip=skip_d, check=False)
     ms_e2e, _, _ = timed(degraded_e2e, skip_d, args.steps, e2e=True, graph=use_graph)
-    e2e_value = tokens_per_step * args.steps / (ms_e2e / 1000.0)
+    e2e_value = tokens_per_step / ((ms_e2e / args.steps) / 1000.0 + refresh_s_per_step)
     h2d = sum(2 * mb.tokens.numel() * 8 for mb in degraded_e2e)
     loss_ok = bool(torch.isfinite(eng.losses).all().item())
 
@@ -417,22 +420,25 @@ def main():
             cpu = {"error": str(exc)}
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps + 1000 * refresh_s_per_step, 3),
+        "value_steady": round(value_steady, 1), "ms_per_step_steady": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision, "impl": "ours",
         "data": "synthetic (uniform tokens in [0,32000), PCG64 seeds 1000+j; weights = reference init_weights seed 0)",
         "config": {"workload": WORKLOAD, "model": "LLaMA-60M", "global_batch": R * SEQS, "seq_len": cfg.seq_len,
                    "microbatch_tokens": b, "logical_ranks": R, "failed_ranks": list(FAILED), "rank_r": RANK,
                    "parallelism": f"dp{world} (MeCeFO ring, NDB neighbour)", "l2": "inputs larger than L2 "
                    "(per-step activations + logits > 126 MB)", "refresh_period": 100},
-        "projection_refresh": {"ms": round(1000 * t_refresh, 1), "refresh_period": eng.tau,
-                               "value_amortized": round(value_amortized, 1),
+        "projection_refresh": {"ms": round(1000 * t_refresh, 2), "refresh_period": eng.tau,
+                               "ms_per_step_amortised": round(1000 * refresh_s_per_step, 3),
                                "note": "batched block power iteration for every lean layer's gate/up/down bases "
-                                       "(30 iterations = costmodel.py:41 charge; fp32 engine GEMMs, CholeskyQR with "
-                                       "k x k factorisations on the host, one round trip per iteration), once per "
-                                       "tau=100 steps; excluded from `value`, included in `value_amortized`"},
+                                       "(30 iterations = costmodel.py:41 charge; one launch per phase for all "
+                                       "matrices, fp64 CholeskyQR and Jacobi Rayleigh-Ritz on the device, "
+                                       "no host round trip), once per tau steps; `value`, `ms_per_step` and "
+                                       "`e2e` include it amortised over tau, `value_steady` does not"},
         "fault_free_tokens_per_s": round(ff_value, 1) if ff_value else None,
         "kernels_fault_free": kernels_ff,
-        "drop_pct_instantaneous": round(100.0 * (1.0 - value / ff_value), 2) if ff_value else None,
+        "drop_pct_instantaneous": round(100.0 * (1.0 - value_steady / ff_value), 2) if ff_value else None,
+        "drop_pct_amortised": round(100.0 * (1.0 - value / ff_value), 2) if ff_value else None,
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4 * R},
         "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,

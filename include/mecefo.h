@@ -240,6 +240,29 @@ int mecefo_gemm(mecefo_engine* e, int64_t M, int64_t N, int64_t K, const void* a
                 const void* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha, float beta,
                 void* stream);
 
+/* One matrix of a batched projection refresh (approx.py:66-87 refreshes
+ * every (layer, kind) basis of a rank at once; each is linalg.py:97-142). */
+typedef struct mecefo_subspace_job {
+  const float* w;  /* rows x cols fp32, row stride ldw */
+  int64_t rows, cols, ldw;
+  int32_t k;       /* block width r + oversample (linalg.py:115), r <= k <= cols */
+  int32_t r;       /* basis rank */
+  float* v;        /* cols x k (ld k) scratch: in = orthonormal start block
+                      (linalg.py:117), out = the iterated orthonormal block */
+  float* v1;       /* cols x r (ld r) out: Ritz vectors of the r largest Ritz
+                      values, descending (linalg.py:124-131) */
+  float* theta;    /* r out (optional, may be NULL): those Ritz values */
+} mecefo_subspace_job;
+
+/* Block power iteration + Rayleigh-Ritz for `count` matrices at once
+ * (linalg.py:119-131 with QR as CholeskyQR: fp32 GEMMs; fp64 k x k Cholesky
+ * and Jacobi eigensolve on the device; no host round trip). `jobs` is a HOST
+ * array. Fixed `iterations` (the budgeted refresh; costmodel.py:41 charges
+ * 30). k <= 512. */
+size_t mecefo_subspace_workspace_bytes(const mecefo_subspace_job* jobs, int32_t count);
+int mecefo_subspace_iteration_batched(mecefo_engine* e, const mecefo_subspace_job* jobs, int32_t count,
+                                      int32_t iterations, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernels this library has launched (evidence counter). */
 int64_t mecefo_launch_count(void);
 

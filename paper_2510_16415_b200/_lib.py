@@ -106,6 +106,20 @@ class AdamSegment(ctypes.Structure):
     ]
 
 
+class SubspaceJob(ctypes.Structure):
+    _fields_ = [
+        ("w", c_void_p),
+        ("rows", c_int64),
+        ("cols", c_int64),
+        ("ldw", c_int64),
+        ("k", c_int32),
+        ("r", c_int32),
+        ("v", c_void_p),
+        ("v1", c_void_p),
+        ("theta", c_void_p),
+    ]
+
+
 # name -> (restype, argtypes)
 _SIGNATURES = {
     "mecefo_last_error": (c_char_p, []),
@@ -181,6 +195,8 @@ _SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int32, c_void_p,
          c_int64, c_float, c_float, c_void_p],
     ),
+    "mecefo_subspace_workspace_bytes": (c_size_t, [c_void_p, c_int32]),
+    "mecefo_subspace_iteration_batched": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_size_t, c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

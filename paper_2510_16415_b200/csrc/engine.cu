@@ -3,6 +3,7 @@
 // steps, and the C-ABI declared in include/mecefo.h.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cmath>
@@ -22,6 +23,7 @@
 #include "gemm_dual.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "subspace.cuh"
 
 using namespace mecefo;
 
@@ -1343,6 +1345,181 @@ int mecefo_gemm(mecefo_engine* e, int64_t M, int64_t N, int64_t K, const void* a
   g.a = {a, lda, a_kmajor != 0}; g.b = {b, ldb, b_kmajor != 0};
   g.epi = epi_store(c, ldc, PREC_F32, alpha, beta);
   return run_gemm(e, g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+namespace {
+struct SubspacePlan {
+  size_t off_b, off_z, off_g, off_m, off_ur, off_th, off_ks, off_jobs, off_scr, total;
+  size_t ritz_bytes, chol_bytes;  // per-matrix scratch (smem or global)
+  int kmax, rmax;
+  bool smem;
+};
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr int SUB_PHASES = 6;
+constexpr int SUB_GRAM_SPLIT = 4;  // split-K of the long-K Gram products (partials summed by their consumers)
+constexpr size_t SUB_SMEM_MAX = 220 * 1024;
+
+SubspacePlan subspace_plan(const mecefo_subspace_job* jobs, int count) {
+  SubspacePlan p{};
+  size_t o = 0, zb = 0, bb = 0;
+  p.kmax = 1;
+  p.rmax = 1;
+  for (int i = 0; i < count; ++i) {
+    bb += al256((size_t)jobs[i].cols * jobs[i].cols * 4);
+    zb += al256((size_t)jobs[i].cols * jobs[i].k * 4);
+    p.kmax = std::max(p.kmax, (int)jobs[i].k);
+    p.rmax = std::max(p.rmax, (int)jobs[i].r);
+  }
+  const size_t kk = (size_t)p.kmax * p.kmax;
+  const size_t kl = (size_t)p.kmax * (p.kmax | 1);  // odd row stride (subspace.cuh sub_ld)
+  p.chol_bytes = (kl + p.kmax) * 8;
+  p.ritz_bytes = kl * 8 + kl * 4;
+  p.off_b = o; o += bb;
+  p.off_z = o; o += zb;
+  p.off_g = o; o += al256(SUB_GRAM_SPLIT * count * kk * 4);
+  p.off_m = o; o += al256(count * kk * 4);
+  p.off_ur = o; o += al256(count * (size_t)p.kmax * p.rmax * 4);
+  p.off_th = o; o += al256(count * (size_t)p.rmax * 4);
+  p.off_ks = o; o += al256(2 * count * 4);
+  p.off_jobs = o; o += al256(sizeof(SubGemmJob) * count * SUB_PHASES);
+  p.smem = std::max(p.chol_bytes, p.ritz_bytes) <= SUB_SMEM_MAX;
+  p.off_scr = o; if (!p.smem) o += al256(count * std::max(p.chol_bytes, p.ritz_bytes));
+  p.total = o;
+  return p;
+}
+
+SubGemmJob sub_job(const float* a, int64_t lda, bool a_kmajor, const float* b, int64_t ldb, float* c, int64_t ldc,
+                   int M, int N, int K) {
+  SubGemmJob j{};
+  j.a = a; j.lda = lda; j.a_kmajor = a_kmajor ? 1 : 0;
+  j.b = b; j.ldb = ldb; j.c = c; j.ldc = ldc;
+  j.M = M; j.N = N; j.K = K;
+  j.tiles_n = (N + SG_TN - 1) / SG_TN;
+  j.tiles_mn = ((M + SG_TM - 1) / SG_TM) * j.tiles_n;
+  j.ksplit = 1;
+  j.kchunk = K;
+  j.c_split = 0;
+  auto al = [](const void* q, int64_t ld) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld & 3) == 0; };
+  j.vec = al(a, lda) && al(b, ldb) ? 1 : 0;
+  return j;
+}
+}  // namespace
+
+size_t mecefo_subspace_workspace_bytes(const mecefo_subspace_job* jobs, int32_t count) {
+  if (!jobs || count < 1) return 0;
+  return subspace_plan(jobs, count).total;
+}
+
+int mecefo_subspace_iteration_batched(mecefo_engine* e, const mecefo_subspace_job* jobs, int32_t count,
+                                      int32_t iterations, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!e) return set_err(MECEFO_ERR_CONTRACT, "null engine");
+  if (!jobs || count < 1) return set_err(MECEFO_ERR_CONTRACT, "subspace iteration needs >= 1 job");
+  if (iterations < 1) return set_err(MECEFO_ERR_CONTRACT, "iterations must be >= 1, got %d", iterations);
+  for (int i = 0; i < count; ++i) {
+    const mecefo_subspace_job& j = jobs[i];
+    if (!j.w || !j.v || !j.v1) return set_err(MECEFO_ERR_CONTRACT, "job %d: null pointer", i);
+    if (j.rows < 1 || j.cols < 1 || j.ldw < j.cols)
+      return set_err(MECEFO_ERR_CONTRACT, "job %d: bad shape %lldx%lld ld %lld", i, (long long)j.rows,
+                     (long long)j.cols, (long long)j.ldw);
+    if (j.r < 1 || j.k < j.r || j.k > j.cols || j.k > 512)
+      return set_err(MECEFO_ERR_CONTRACT, "job %d: need 1 <= r=%d <= k=%d <= min(cols=%lld, 512)", i, j.r, j.k,
+                     (long long)j.cols);
+    if (j.cols > 46340 || j.rows > (int64_t)1 << 30) return set_err(MECEFO_ERR_CONTRACT, "job %d: too large", i);
+  }
+  const SubspacePlan p = subspace_plan(jobs, count);
+  if (!workspace || workspace_bytes < p.total)
+    return set_err(MECEFO_ERR_CONTRACT, "subspace workspace too small: %zu < %zu", workspace_bytes, p.total);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  const int kmax = p.kmax, rmax = p.rmax;
+  const size_t kk = (size_t)kmax * kmax;
+  float* G = reinterpret_cast<float*>(ws + p.off_g);
+  float* Mm = reinterpret_cast<float*>(ws + p.off_m);
+  float* Ur = reinterpret_cast<float*>(ws + p.off_ur);
+  float* Th = reinterpret_cast<float*>(ws + p.off_th);
+  // phases: 0 B = W^T W, 1 Z = B V, 2 G = Z^T Z, 3 V = Z M, 4 S = V^T Z (into G), 5 V1 = V Ur
+  std::vector<SubGemmJob> hj((size_t)count * SUB_PHASES);
+  std::vector<int> hk(2 * count);
+  int tiles[SUB_PHASES] = {};
+  size_t ob = p.off_b, oz = p.off_z;
+  for (int i = 0; i < count; ++i) {
+    const mecefo_subspace_job& j = jobs[i];
+    const int n = (int)j.cols, k = j.k, r = j.r, rows = (int)j.rows;
+    float* B = reinterpret_cast<float*>(ws + ob); ob += al256((size_t)n * n * 4);
+    float* Z = reinterpret_cast<float*>(ws + oz); oz += al256((size_t)n * k * 4);
+    float* g = G + i * kk;
+    float* m = Mm + i * kk;
+    SubGemmJob ph[SUB_PHASES] = {
+        sub_job(j.w, j.ldw, false, j.w, j.ldw, B, n, n, n, rows),
+        sub_job(B, n, true, j.v, k, Z, k, n, k, n),
+        sub_job(Z, k, false, Z, k, g, kmax, k, k, n),
+        sub_job(Z, k, true, m, kmax, j.v, k, n, k, k),
+        sub_job(j.v, k, false, Z, k, g, kmax, k, k, n),
+        sub_job(j.v, k, true, Ur + (size_t)i * kmax * rmax, r, j.v1, r, n, r, k),
+    };
+    for (int q : {2, 4}) {  // Gram products: K = cols >> k
+      ph[q].ksplit = SUB_GRAM_SPLIT;
+      ph[q].kchunk = ((n + SUB_GRAM_SPLIT - 1) / SUB_GRAM_SPLIT + SG_TK - 1) / SG_TK * SG_TK;
+      ph[q].c_split = (int64_t)count * kk;
+    }
+    for (int q = 0; q < SUB_PHASES; ++q) {
+      ph[q].tile0 = tiles[q];
+      tiles[q] += ph[q].tiles_mn * ph[q].ksplit;
+      hj[(size_t)q * count + i] = ph[q];
+    }
+    hk[i] = k;
+    hk[count + i] = r;
+  }
+  SubGemmJob* dj = reinterpret_cast<SubGemmJob*>(ws + p.off_jobs);
+  int* dk = reinterpret_cast<int*>(ws + p.off_ks);
+  // pageable sources: the copies are staged before these calls return
+  CUDA_TRY(cudaMemcpyAsync(dj, hj.data(), hj.size() * sizeof(SubGemmJob), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(dk, hk.data(), hk.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  static bool configured = false;
+  if (!configured) {
+    CUDA_TRY(cudaFuncSetAttribute(subspace_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SUB_SMEM_MAX));
+    CUDA_TRY(cudaFuncSetAttribute(subspace_ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SUB_SMEM_MAX));
+    configured = true;
+  }
+  void* scratch = p.smem ? nullptr : ws + p.off_scr;
+  const size_t scr_stride = std::max(p.chol_bytes, p.ritz_bytes);
+  static const char* const phase_tag[SUB_PHASES] = {"subspace.gram_w", "subspace.bv", "subspace.gram_z",
+                                                     "subspace.zm", "subspace.vtz", "subspace.rotate"};
+  auto gemm_phase = [&](int q) -> int {
+    ProfScope ps(phase_tag[q], 0.0, 0.0, s);
+    subspace_gemm_kernel<<<tiles[q], SG_THREADS, 0, s>>>(dj + (size_t)q * count, count);
+    return check_launch("subspace_gemm_kernel");
+  };
+  TRY(gemm_phase(0));
+  for (int it = 0; it < iterations; ++it) {
+    TRY(gemm_phase(1));
+    TRY(gemm_phase(2));
+    {
+      ProfScope ps("subspace.chol", 0.0, 0.0, s);
+      // the global-scratch layout uses the same per-matrix stride as the Ritz step
+      subspace_chol_inv_kernel<<<count, SUB_SMALL_THREADS, p.smem ? p.chol_bytes : 0, s>>>(
+          G, Mm, dk, kmax, static_cast<double*>(scratch), p.smem ? 1 : 0, scr_stride / 8, SUB_GRAM_SPLIT,
+          (size_t)count * kk);
+      TRY(check_launch("subspace_chol_inv_kernel"));
+    }
+    TRY(gemm_phase(3));
+  }
+  TRY(gemm_phase(1));
+  TRY(gemm_phase(4));
+  {
+    ProfScope ps("subspace.ritz", 0.0, 0.0, s);
+    subspace_ritz_kernel<<<count, SUB_SMALL_THREADS, p.smem ? p.ritz_bytes : 0, s>>>(G, Ur, Th, dk, dk + count, kmax, rmax, scratch,
+                                                                     scr_stride, p.smem ? 1 : 0, SUB_GRAM_SPLIT,
+                                                                     (size_t)count * kk);
+    TRY(check_launch("subspace_ritz_kernel"));
+  }
+  TRY(gemm_phase(5));
+  for (int i = 0; i < count; ++i)
+    if (jobs[i].theta)
+      CUDA_TRY(cudaMemcpyAsync(jobs[i].theta, Th + (size_t)i * rmax, jobs[i].r * 4, cudaMemcpyDeviceToDevice, s));
+  return MECEFO_OK;
 }
 
 }  // extern "C"

@@ -143,75 +143,54 @@ def _start_block(n: int, k: int, seed: int, device) -> torch.Tensor:
     return _START_CACHE[key]
 
 
-def top_r_right_singular_vectors_batched(ws: list, ranks: list, iterations: int, seed: int) -> list:
+def top_r_right_singular_vectors_batched(ws: list, ranks: list, iterations: int, seed: int,
+                                         return_values: bool = False):
     """Budgeted block power iteration for many matrices at once (the
     tau-amortised projection refresh of every due (rank, layer, kind)).
 
-    Same iteration as linalg.py:97-142 with two changes that keep it on the
-    GPU: QR is CholeskyQR (Gram matrix on the engine, k x k Cholesky on the
-    host, one batched round trip per iteration for ALL matrices), and the
-    Rayleigh-Ritz rotation is applied once at the end (it only reorders the
-    spanned subspace). Runs a fixed number of iterations (the reference cost
-    model charges SVD_CHARGED_ITERATIONS = 30, costmodel.py:41); used for
-    throughput runs. Parity tests inject the reference's converged bases."""
+    Same iteration as linalg.py:97-142 — start block linalg.py:117, Z = B V,
+    re-orthonormalise, Rayleigh-Ritz (linalg.py:124-129), keep the top r —
+    with two changes that keep it entirely on the GPU: QR is CholeskyQR
+    (fp32 Gram matrix, fp64 k x k Cholesky and triangular inverse on the
+    device) and the Ritz rotation (fp64 Jacobi eigensolve on the device) is
+    taken once at the end, since it only rotates within the spanned
+    subspace. One launch per phase for ALL matrices, no host round trip
+    (mecefo_subspace_iteration_batched). Runs a fixed number of iterations
+    (the reference cost model charges SVD_CHARGED_ITERATIONS = 30,
+    costmodel.py:41); used for throughput runs. Parity tests inject the
+    reference's converged bases."""
+    from . import _lib
+
     if not ws:
-        return []
+        return ([], []) if return_values else []
     eng = _fp32_engine()
     dev = ws[0].device if ws[0].is_cuda else torch.device("cuda")
-    Bs, Vs, Zs, ks = [], [], [], []
-    for w, r in zip(ws, ranks):
-        wd = w.detach().to(device=dev, dtype=torch.float32).contiguous()
-        n = wd.shape[1]
-        B = torch.empty(n, n, dtype=torch.float32, device=dev)
-        runtime.gemm(eng, wd, False, wd, False, n, n, wd.shape[0], B)  # W^T W
+    jobs = (_lib.SubspaceJob * len(ws))()
+    keep, outs, thetas = [], [], []
+    for i, (w, r) in enumerate(zip(ws, ranks)):
+        wd = w.detach()
+        if wd.device != dev or wd.dtype != torch.float32 or wd.stride(1) != 1:
+            wd = wd.to(device=dev, dtype=torch.float32).contiguous()
+        rows, n = wd.shape
+        if not 1 <= r <= n:
+            raise ContractViolation(f"rank {r} outside [1, {n}] for shape {tuple(wd.shape)}")
         k = min(n, r + _OVERSAMPLE)
-        Bs.append(B)
-        Vs.append(_start_block(n, k, seed, dev).clone())
-        Zs.append(torch.empty(n, k, dtype=torch.float32, device=dev))
-        ks.append(k)
-    kmax = max(ks)
-    G = torch.zeros(len(ws), kmax, kmax, dtype=torch.float32, device=dev)
-    M = torch.zeros(len(ws), kmax, kmax, dtype=torch.float32, device=dev)
-    for _ in range(iterations):
-        for i, (B, V, Z, k) in enumerate(zip(Bs, Vs, Zs, ks)):
-            n = B.shape[0]
-            runtime.gemm(eng, B, True, V, False, n, k, n, Z)            # Z = B V
-            g = G[i, :k, :k]
-            _lib_gemm_into(eng, Z, Z, k, k, n, g)                         # G = Z^T Z
-        Gh = G.double().cpu().numpy()
-        for i, k in enumerate(ks):  # pad smaller blocks with identity
-            if k < kmax:
-                Gh[i, k:, :] = 0.0
-                Gh[i, :, k:] = 0.0
-                Gh[i, range(k, kmax), range(k, kmax)] = 1.0
-        Gh = 0.5 * (Gh + np.transpose(Gh, (0, 2, 1)))
-        try:  # one batched LAPACK call for all matrices
-            L = np.linalg.cholesky(Gh)
-        except np.linalg.LinAlgError:  # a rank-deficient block: regularise all
-            tr = np.trace(Gh, axis1=1, axis2=2)[:, None, None] / kmax
-            L = np.linalg.cholesky(Gh + 1e-12 * tr * np.eye(kmax))
-        Mh = np.transpose(np.linalg.inv(L), (0, 2, 1))                      # Q = Z L^{-T}
-        M.copy_(torch.from_numpy(np.ascontiguousarray(Mh, dtype=np.float32)))
-        for i, (V, Z, k) in enumerate(zip(Vs, Zs, ks)):
-            n = Z.shape[0]
-            mk = M[i, :k, :k].contiguous()
-            runtime.gemm(eng, Z, True, mk, False, n, k, k, V)            # V = Z M
-    # Rayleigh-Ritz: S = V^T B V, eigh on the host, V1 = V U[:, :r] (descending)
-    for i, (B, V, Z, k) in enumerate(zip(Bs, Vs, Zs, ks)):
-        n = B.shape[0]
-        runtime.gemm(eng, B, True, V, False, n, k, n, Z)
-        _lib_gemm_into(eng, V, Z, k, k, n, G[i, :k, :k])
-    Sh = G.double().cpu().numpy()
-    out = []
-    for i, (V, r, k) in enumerate(zip(Vs, ranks, ks)):
-        s = 0.5 * (Sh[i, :k, :k] + Sh[i, :k, :k].T)
-        theta, U = np.linalg.eigh(s)
-        U = U[:, np.argsort(theta)[::-1][:r]]
-        Ud = torch.from_numpy(np.ascontiguousarray(U, dtype=np.float32)).to(dev)
-        v1 = torch.empty(V.shape[0], r, dtype=torch.float32, device=dev)
-        runtime.gemm(eng, V, True, Ud, False, V.shape[0], r, k, v1)
-        out.append(v1)
-    return out
+        V = _start_block(n, k, seed, dev).clone()
+        v1 = torch.empty(n, r, dtype=torch.float32, device=dev)
+        th = torch.empty(r, dtype=torch.float32, device=dev) if return_values else None
+        jobs[i] = _lib.SubspaceJob(wd.data_ptr(), rows, n, wd.stride(0), k, r, V.data_ptr(), v1.data_ptr(),
+                                   th.data_ptr() if th is not None else None)
+        keep += [wd, V]
+        outs.append(v1)
+        thetas.append(th)
+    nbytes = _lib.load().mecefo_subspace_workspace_bytes(jobs, len(ws))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _lib.call("mecefo_subspace_iteration_batched", eng.handle, jobs, len(ws), iterations, scratch.data_ptr(), nbytes,
+              runtime.stream_ptr())
+    # the caching allocator may hand `scratch`/`keep` to later work on this
+    # stream only after the queued kernels, so no synchronisation is needed
+    del keep, scratch
+    return (outs, thetas) if return_values else outs
 
 
 def _lib_gemm_into(eng, X, Y, rows, cols, inner, out):

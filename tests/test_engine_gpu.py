@@ -180,20 +180,28 @@ def test_batched_refresh_finds_dominant_subspace(cuda):
 
     rng = np.random.Generator(np.random.PCG64(3))
     mats, refs = [], []
-    for (out, n, r) in ((344, 128, 32), (128, 344, 32), (512, 256, 64)):
+    # odd k (r=33), k == cols (20 x 18), and the C1 down-projection shape
+    for (out, n, r) in ((344, 128, 32), (128, 344, 33), (512, 256, 64), (40, 20, 18), (512, 1376, 128)):
         q = min(out, n)
         u, _ = np.linalg.qr(rng.normal(size=(out, q)))
         v, _ = np.linalg.qr(rng.normal(size=(n, q)))
         s = np.concatenate([np.linspace(10, 5, r), np.linspace(1, 0.1, q - r)])
         w = (u * s) @ v.T
         mats.append(torch.tensor(w, dtype=torch.float32, device="cuda"))
-        refs.append((np.linalg.svd(w)[2][:r].T, r))
-    got = top_r_right_singular_vectors_batched(mats, [r for _, r in refs], iterations=30, seed=23)
-    for v1, (vref, r) in zip(got, refs):
+        refs.append((v[:, :r], s[:r], r))
+    got, theta = top_r_right_singular_vectors_batched(mats, [r for *_, r in refs], iterations=30, seed=23,
+                                                      return_values=True)
+    for v1, th, (vref, sref, r) in zip(got, theta, refs):
         v1 = v1.double().cpu().numpy()
+        th = th.double().cpu().numpy()
         assert v1.shape == vref.shape
         assert np.abs(v1.T @ v1 - np.eye(r)).max() < 1e-4
         assert np.abs(v1 @ v1.T - vref @ vref.T).max() < 1e-3
+        # Ritz values: descending, = sigma^2 (linalg.py:127-129)
+        assert np.all(np.diff(th) <= 0)
+        assert np.abs(th - sref ** 2).max() < 1e-3 * sref[0] ** 2
+        # each Ritz vector matches its singular vector up to sign
+        assert np.abs(np.abs(np.sum(v1 * vref, axis=0)) - 1).max() < 1e-3
 
 
 def test_engine_budgeted_refresh_runs_and_is_shared(cuda):
