@@ -209,7 +209,7 @@ def load(path: str | None = None):
     global _LIB
     if _LIB is not None:
         return _LIB
-    p = path or LIB_PATH
+    p = path or os.environ.get("MECEFO_LIB") or LIB_PATH  # MECEFO_LIB: A/B a second in-tree build
     if not os.path.exists(p):
         raise EngineUnavailable(
             f"{LIB_NAME} not found at {p}; build it with `python -c 'import __graft_entry__ as g; g.build()'`"

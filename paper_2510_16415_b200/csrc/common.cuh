@@ -80,7 +80,15 @@ __device__ __forceinline__ float block_max(float v, float* red) {
 
 // SiLU and its derivative, same formulas as the reference
 // (pkg/src/faultsim/model.py:198-204), evaluated in fp32.
-__device__ __forceinline__ float sigmoid_f(float z) { return __frcp_rn(1.f + __expf(-z)); }
+// rcp.approx (1 ulp) instead of the IEEE-rounded reciprocal: no slow-path
+// branch in the SwiGLU epilogues; inf -> 0 and 1 -> 1 stay exact.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sigmoid_f(float z) { return rcp_approx(1.f + __expf(-z)); }
+__device__ __forceinline__ float sigmoid_ieee_f(float z) { return __frcp_rn(1.f + __expf(-z)); }
 __device__ __forceinline__ float silu_f(float z) { return z * sigmoid_f(z); }
 __device__ __forceinline__ float silu_grad_f(float z) {
   const float s = sigmoid_f(z);

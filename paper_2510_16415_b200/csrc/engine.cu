@@ -314,6 +314,12 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     outs.prec[k] = slots[k].prec;
     outs.reduce[k] = slots[k].reduce;
   }
+  {  // timing experiments only: MECEFO_DBG_NOEPI drops every output, MECEFO_DBG_NOROPE the rotation
+    static const bool no_epi = getenv("MECEFO_DBG_NOEPI") != nullptr;
+    static const bool no_rope = getenv("MECEFO_DBG_NOROPE") != nullptr;
+    if (no_epi) outs.used[0] = outs.used[1] = outs.used[2] = 0;
+    if (no_rope) p.epi.rope_cos = nullptr;
+  }
   auto kern = gemm_tc_kernel<BN, AK, BKM, CL>;
   static bool attr_set = false;
   if (!attr_set) {

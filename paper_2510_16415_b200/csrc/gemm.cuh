@@ -307,6 +307,17 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t tmem_d, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -380,14 +391,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   tmem_ld16(taddr + 16, v + 16);
 }
 
-// One warp writes its 32 rows x 32 columns to the staging buffer in the TMA
-// swizzle layout (fp32: 128-B rows, SWIZZLE_128B; bf16: 64-B rows,
-// SWIZZLE_64B) and lane 0 issues the bulk store / reduce-add.
-// Epilogue staging, in 16-column halves of a 32-column chunk so the live
-// register set stays small (no spills at the 168-register cap of 384
-// threads). Layout = the TMA swizzle of the store map: fp32 -> 128-B rows,
-// SWIZZLE_128B; bf16 -> 64-B rows, SWIZZLE_64B.
-__device__ __forceinline__ void stage_wait(int lane) {
+// Epilogue staging: each epilogue warp owns a 4 KB box holding its 32 rows x
+// one 32-column chunk in the TMA swizzle layout of the store map (fp32: 128-B
+// rows, SWIZZLE_128B; bf16: 64-B rows, SWIZZLE_64B), written in 16-column
+// halves; lane 0 issues the bulk store / reduce-add. (A double-buffered box
+// per warp measured 2-4% slower: the extra outstanding bulk stores cost more
+// than the read-completion wait they hide.)
+__device__ __forceinline__ void stage_wait(int lane) {  // previous store has read the box
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   __syncwarp();
 }
@@ -430,6 +440,20 @@ __device__ __forceinline__ void stage_store32(uint8_t* stg, const CUtensorMap* m
   stage_commit(stg, map, reduce, c0, r0, lane);
 }
 
+// bf16 32-column box (32 rows x 64 B = 2 KB) through one of the two halves
+// of the warp's 4 KB staging buffer: only the store before last must have
+// read its half.
+__device__ __forceinline__ void stage_store32_db(uint8_t* stg, int& sb, const CUtensorMap* map, const float* v,
+                                                 int c0, int r0, int lane) {
+  uint8_t* box = stg + sb * 2048;
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+  stage_write16(box, v, PREC_BF16, 0, lane);
+  stage_write16(box, v + 16, PREC_BF16, 1, lane);
+  stage_commit(box, map, 0, c0, r0, lane);
+  sb ^= 1;
+}
+
 // Epilogue math for output slot `slot` on 16 consecutive output columns n0..
 // of row r (tcgen05 path): 0 = out / act, 1 = gate or d_gate, 2 = up or d_up.
 __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, int n0, int cnt, bool row_ok,
@@ -440,21 +464,26 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
     if (e.rope_cos && n0 < e.rope_cols && row_ok) {
       const int pos = r % e.rope_T, half = e.rope_hd >> 1;
       if ((e.rope_hd & 15) == 0 && n0 + 16 <= e.rope_cols) {
-        // the 16-column span lies inside one head: 8 consecutive (cos, sin)
-        const int base = pos * half + ((n0 % e.rope_hd) >> 1);
-        float cs[8], sn[8];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const float4 c4 = __ldg(reinterpret_cast<const float4*>(e.rope_cos + base) + q);
-          const float4 s4 = __ldg(reinterpret_cast<const float4*>(e.rope_sin + base) + q);
-          cs[4 * q] = c4.x; cs[4 * q + 1] = c4.y; cs[4 * q + 2] = c4.z; cs[4 * q + 3] = c4.w;
-          sn[4 * q] = s4.x; sn[4 * q + 1] = s4.y; sn[4 * q + 2] = s4.z; sn[4 * q + 3] = s4.w;
-        }
+        // The 16-column span lies inside one head: 8 consecutive frequencies.
+        // The angles are computed, not looked up — the cos/sin table does
+        // not stay L1-resident next to a 224 KB operand ring, and its L2
+        // latency was serialising the epilogue. theta_j = 10000^(-2j/hd)
+        // (model.py:274); |angle error| <= ~6e-5 rad after Cody-Waite
+        // reduction to [-pi, pi], far below the bf16 rounding of q/k.
+        const int j0 = (n0 % e.rope_hd) >> 1;
+        const float ls = -26.575424759098898f / (float)e.rope_hd;  // -2 log2(10000) / hd
+        const float fpos = (float)pos;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
+          const float ang = fpos * exp2f((float)(j0 + j) * ls);
+          const float kq = rintf(ang * 0.15915494309189535f);
+          float rr = fmaf(-kq, 6.28318548202514648f, ang);
+          rr = fmaf(kq, 1.7484556e-7f, rr);
+          float sn, cs;
+          __sincosf(rr, &sn, &cs);
           const float ev = o[2 * j], od = o[2 * j + 1];
-          o[2 * j] = ev * cs[j] - od * sn[j];
-          o[2 * j + 1] = ev * sn[j] + od * cs[j];
+          o[2 * j] = ev * cs - od * sn;
+          o[2 * j + 1] = ev * sn + od * cs;
         }
       } else {
 #pragma unroll
@@ -673,28 +702,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const bool row_ok = row < p.M;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
+      const int cbase = p.paired ? nt * (BN / 2) : nt * BN;
+      bool released = false;
 #pragma unroll 1
       for (int c = half; c < nchunks; c += 2) {
-        const int n0 = (p.paired ? nt * (BN / 2) : nt * BN) + c * 32;
+        const int n0 = cbase + c * 32;
         if (n0 >= p.N) continue;  // warp-uniform
-#pragma unroll 1
-        for (int slot = 0; slot < 3; ++slot) {
+        // all TMEM columns of the chunk in flight before one wait::ld
+        float g[32], u[32];
+        tmem_ld16_nowait(taddr + c * 32, g);
+        tmem_ld16_nowait(taddr + c * 32 + 16, g + 16);
+        if (p.paired) {
+          tmem_ld16_nowait(taddr + BN / 2 + c * 32, u);
+          tmem_ld16_nowait(taddr + BN / 2 + c * 32 + 16, u + 16);
+        }
+        tmem_wait_ld();
+        if (c + 2 >= nchunks || cbase + (c + 2) * 32 >= p.N) {
+          // this warp's last chunk is in registers: hand the accumulator
+          // back to the MMA warp before the math and stores
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          released = true;
+        }
+#pragma unroll
+        for (int slot = 0; slot < 3; ++slot) {  // unrolled: outs.* indexed statically (no local-memory copy)
           if (!outs.used[slot]) continue;
           stage_wait(lane);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            float g[16], u[16], o[16];
-            tmem_ld16(taddr + c * 32 + hh * 16, g);
-            if (p.paired) tmem_ld16(taddr + BN / 2 + c * 32 + hh * 16, u);
+            float o[16];
             const int n0h = n0 + hh * 16;
-            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g, u, o);
+            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g + hh * 16, u + hh * 16, o);
             stage_write16(stg, o, outs.prec[slot], hh, lane);
           }
           stage_commit(stg, slot == 0 ? &tmO0 : (slot == 1 ? &tmO1 : &tmO2), outs.reduce[slot], n0, r0, lane);
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (!released) {
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
