@@ -242,6 +242,9 @@ struct GemmCall {
   int split = 1;
   const char* tag = "gemm";
   int force_bn = 0;  // tcgen05 tile width override (split-K accumulate GEMMs)
+  // block-diagonal batching: M tile mt reads B columns shifted by mt * b_diag_off
+  // (two independent products sharing one launch; needs 128-row blocks)
+  int64_t b_diag_off = 0;
 };
 
 Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, float beta = 0.f,
@@ -259,13 +262,14 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   CUtensorMap ta, tb;
   if (AK) TRY(make_tmap(e, &ta, g.a.p, g.K, g.M, g.a.ld, 64, TC_BM));
   else TRY(make_tmap(e, &ta, g.a.p, g.M, g.K, g.a.ld, 64, 64));
-  const int64_t rowsB = g.paired ? g.pair_off + g.N : g.N;
+  const int64_t rowsB = g.paired ? g.pair_off + g.N : g.N + g.b_diag_off * ((g.M + TC_BM - 1) / TC_BM - 1);
   if (BKM) TRY(make_tmap(e, &tb, g.b.p, g.K, rowsB, g.b.ld, 64, (g.paired || CL > 1) ? BN / 2 : BN));
   else TRY(make_tmap(e, &tb, g.b.p, rowsB, g.K, g.b.ld, 64, 64));
   GemmDev p{};
   p.M = (int)g.M; p.N = (int)g.N; p.K = (int)g.K;
   p.paired = g.paired ? 1 : 0;
   p.pair_off = g.pair_off;
+  p.b_diag_off = g.b_diag_off;
   p.kblocks = (int)((g.K + TC_BK - 1) / TC_BK);
   int split = std::max(1, std::min(g.split, p.kblocks));
   p.kb_per_split = (p.kblocks + split - 1) / split;
@@ -362,7 +366,7 @@ int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
 // Measured: pays off only for very large tile counts (the LM-head GEMMs,
 // +10%); neutral-to-negative on the per-layer GEMMs.
 bool use_cluster(const GemmCall& g, int BN) {
-  if (getenv("MECEFO_NO_CLUSTER")) return false;
+  if (getenv("MECEFO_NO_CLUSTER") || g.b_diag_off) return false;  // the pair shares ONE B tile
   const int64_t cpt = g.paired ? BN / 2 : BN;
   const int64_t tiles = ((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt);
   return BN >= 128 && (g.M + 127) / 128 >= 2 && tiles >= 1024;
@@ -409,6 +413,8 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
                  (double)e->ps * ((double)g.M * g.K + ncols * g.K) + out_bytes * (double)g.M * (double)g.N, s);
   if (g.split > 1 && g.epi.kind != EPI_ATOMIC)
     return set_err(MECEFO_ERR_CONSISTENCY, "split-K requires the atomic epilogue");
+  if (g.b_diag_off && (e->prec != PREC_BF16 || g.paired))
+    return set_err(MECEFO_ERR_CONSISTENCY, "block-diagonal batching is a tcgen05 (bf16), unpaired mode");
   if (e->prec == PREC_BF16) {
     if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
     const int BN = choose_bn(g);
@@ -449,7 +455,8 @@ int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float
     Epilogue ep{};
     ep.kind = EPI_ATOMIC; ep.out = out; ep.ldo = ldo; ep.alpha = alpha; ep.out_prec = PREC_F32;
     g.epi = ep;
-    g.split = std::max(1, std::min((kNumSMs + tiles - 1) / tiles, kblocks / 4));
+    // floor: tiles x split must fit ONE wave (148 CTAs), a 149th CTA doubles the time
+    g.split = std::max(1, std::min(kNumSMs / tiles, kblocks / 4));
     if (e->prec == PREC_F32) g.split = std::max(1, std::min(g.split * 4, (int)((g.K + 15) / 16) / 8));
   } else {
     g.epi = epi_store(out, ldo, PREC_F32, alpha, 1.f);
@@ -561,14 +568,39 @@ int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const vo
   p.tiles_n = (int)((f + DU_NP - 1) / DU_NP);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.has_act = act ? 1 : 0;
+  // pairs of column tiles share the token operands (multicast); an odd last
+  // column tile computes a zero-padded (TMA OOB) neighbour whose stores are skipped
+  static const bool no_cluster = getenv("MECEFO_NO_CLUSTER") != nullptr;
+  const int CL = (!no_cluster && p.num_tiles >= 2 * kNumSMs) ? 2 : 1;
+  p.tiles_n_cl = (p.tiles_n + CL - 1) / CL;
+  p.num_tiles_cl = p.tiles_m * p.tiles_n_cl;
   static bool set = false;
   if (!set) {
-    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
     set = true;
   }
-  CUDA_TRY(pdl_launch(swiglu_bwd_dual_kernel, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), DU_SMEM, s, tdy, th2, twd, twgu, tact, tdg,
-                                                                                     tdu, p));
-  return check_launch("swiglu_bwd_dual_kernel");
+  if (CL == 1) {
+    CUDA_TRY(pdl_launch(swiglu_bwd_dual_kernel<1>, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), DU_SMEM, s,
+                        tdy, th2, twd, twgu, tact, tdg, tdu, p));
+    return check_launch("swiglu_bwd_dual_kernel");
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(CL * std::min(p.num_tiles_cl, kNumSMs / CL)));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = DU_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, swiglu_bwd_dual_kernel<2>, tdy, th2, twd, twgu, tact, tdg, tdu, p));
+  return check_launch("swiglu_bwd_dual_kernel<cluster>");
 }
 
 int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cudaStream_t s) {
@@ -844,6 +876,68 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
   float* Q;
   void* Qc;
   TRY(ws.take(b * 2 * rp * ps, &P));
+  if (e->prec == PREC_BF16 && rp % TC_BM == 0 && kinds[0].grad && kinds[1].grad && pj->v1_gu && pj->v1t_gu &&
+      pj->v1[2] && pj->v1t[2]) {
+    // Transposed chain (bf16, rank_pad a multiple of the 128-row tile):
+    //   [P_g | P_u]   = h2 [V1_g | V1_u]                              (b, 2rp)
+    //   [Q_g^T ; Q_u^T] = [P_g | P_u]^T [d_gate | d_up], block-diagonal:
+    //                   M tile 0 (P_g^T) meets d_gate, tile 1 (P_u^T) d_up (2rp, f)
+    //   [G_g ; G_u]  += alpha blockdiag(Q) [V1_g | V1_u]^T              (2f, m)
+    //   down:  Q_d^T = P_d^T dy (rp, m);  G_d += alpha Q_d V1_d^T      (m, f)
+    // The long-K contraction runs with the token dim as K and the wide
+    // FFN dim as N (256-column tiles), no wasted off-diagonal blocks.
+    float* QT;
+    void* QTc;
+    TRY(ws.take(2 * rp * f * 4, reinterpret_cast<void**>(&QT)));
+    TRY(ws.take(2 * rp * 2 * f * ps, &QTc));
+    GemmCall g;
+    g.M = b; g.N = 2 * rp; g.K = m;
+    g.a = {h2, m, true}; g.b = {pj->v1t_gu, m, true};
+    g.epi = epi_store(P, 2 * rp, e->prec);
+    g.tag = "lowrank.P";
+    TRY(run_gemm(e, g, s));
+    CUDA_TRY(cudaMemsetAsync(QT, 0, 2 * rp * f * 4, s));
+    g = GemmCall();
+    g.M = 2 * rp; g.N = f; g.K = b;
+    g.a = {P, 2 * rp, false}; g.b = {dcat, 2 * f, false};
+    g.b_diag_off = f;
+    g.tag = "lowrank.Q_gu";
+    TRY(gemm_accumulate(e, g, QT, f, 1.f, s));
+    {
+      const int64_t n = 2 * rp * 2 * f;
+      ProfScope prof("lowrank.cast", 0.0, 6.0 * n / 2, s);
+      CUDA_TRY(pdl_launch(cast_blockdiag_t_kernel, dim3((unsigned)std::min<int64_t>((n + 255) / 256, 4 * kNumSMs)),
+                          dim3(256), 0, s, (const float*)QT, (__nv_bfloat16*)QTc, (int)rp, (int)f));
+      TRY(check_launch("cast_blockdiag_t_kernel"));
+    }
+    g = GemmCall();
+    g.M = 2 * f; g.N = m; g.K = 2 * rp;
+    g.a = {QTc, 2 * f, false}; g.b = {pj->v1_gu, 2 * rp, true};
+    g.epi = epi_store(gr->gu, m, PREC_F32, gr->alpha_ffn, 1.f);
+    g.tag = "lowrank.up_proj";
+    TRY(run_gemm(e, g, s));
+    if (!kinds[2].grad) return MECEFO_OK;
+    // down: P_d = act V1_d (b, rp) into the P buffer (stream-ordered reuse)
+    g = GemmCall();
+    g.M = b; g.N = rp; g.K = f;
+    g.a = {act, f, true}; g.b = {pj->v1t[2], f, true};
+    g.epi = epi_store(P, rp, e->prec);
+    g.tag = "lowrank.P_down";
+    TRY(run_gemm(e, g, s));
+    CUDA_TRY(cudaMemsetAsync(QT, 0, rp * m * 4, s));
+    g = GemmCall();
+    g.M = rp; g.N = m; g.K = b;
+    g.a = {P, rp, false}; g.b = {dy_c, m, false};
+    g.tag = "lowrank.Q_down";
+    TRY(gemm_accumulate(e, g, QT, m, 1.f, s));
+    TRY(cast_to_compute(e, QT, QTc, rp * m, s));
+    g = GemmCall();
+    g.M = m; g.N = f; g.K = rp;
+    g.a = {QTc, m, false}; g.b = {pj->v1[2], rp, true};
+    g.epi = epi_store(kinds[2].grad, f, PREC_F32, gr->alpha_ffn, 1.f);
+    g.tag = "lowrank.up_proj";
+    return run_gemm(e, g, s);
+  }
   TRY(ws.take(std::max(m, f) * rp * 4, reinterpret_cast<void**>(&Q)));
   if (e->prec == PREC_BF16) TRY(ws.take(std::max(m, f) * rp * ps, &Qc));
   else Qc = Q;

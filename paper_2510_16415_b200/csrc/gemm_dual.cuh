@@ -11,6 +11,12 @@
 // and d_up = d_act*silu(gate) through swizzled smem + TMA stores. gate, up and
 // d_act never touch HBM, and no epilogue operand is read from
 // global memory.
+//
+// The narrow tile (64 pair columns) re-reads the token operands dy, h2 once
+// per column tile; at ~56 flop per L2 byte that made the kernel L2->SM
+// bandwidth bound. With CL = 2 the CTAs of a cluster take the SAME token
+// tile and neighbouring column tiles: each loads one of dy / h2 and
+// multicasts it to both, halving the token-operand traffic.
 #pragma once
 #include "gemm.cuh"
 
@@ -28,9 +34,11 @@ struct DualDev {
   int M, NP, K;     // tokens, FFN width f, hidden m
   int64_t f_off;    // row offset of W_up inside W_gu (= f)
   int kblocks, tiles_m, tiles_n, num_tiles;
+  int tiles_n_cl, num_tiles_cl;  // column tiles / tiles in units of clusters
   int has_act;
 };
 
+template <int CL>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     swiglu_bwd_dual_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmH2,
                            const __grid_constant__ CUtensorMap tmWd, const __grid_constant__ CUtensorMap tmWgu,
@@ -49,7 +57,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < DU_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // both CTAs' MMAs must release a stage the peer multicasts into
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -65,23 +73,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
   griddep_wait();  // predecessor outputs are visible from here on
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int cl_id = blockIdx.x / CL, n_cl = gridDim.x / CL;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int mt = t % p.tiles_m, nt = t / p.tiles_m;
+      for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
+        const int mt = t % p.tiles_m, nt = (t / p.tiles_m) * CL + crank;
         for (int kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], DU_STAGE_BYTES);
           uint8_t* st = smem + stage * DU_STAGE_BYTES;
           const int k0 = kb * TC_BK;
-          tma_load_2d(st, &tmDy, &full[stage], k0, mt * TC_BM);
-          tma_load_2d(st + DU_A_BYTES, &tmH2, &full[stage], k0, mt * TC_BM);
+          if (CL == 1) {
+            tma_load_2d(st, &tmDy, &full[stage], k0, mt * TC_BM);
+            tma_load_2d(st + DU_A_BYTES, &tmH2, &full[stage], k0, mt * TC_BM);
+          } else if (crank == 0) {  // dy for both CTAs of the pair
+            tma_load_2d_mc(st, &tmDy, &full[stage], k0, mt * TC_BM, kMask);
+          } else {                  // h2 for both
+            tma_load_2d_mc(st + DU_A_BYTES, &tmH2, &full[stage], k0, mt * TC_BM, kMask);
+          }
           tma_load_2d(st + 2 * DU_A_BYTES, &tmWd, &full[stage], nt * DU_NP, k0);
           uint8_t* b2 = st + 2 * DU_A_BYTES + DU_B1_BYTES;
           tma_load_2d(b2, &tmWgu, &full[stage], k0, nt * DU_NP);
@@ -99,7 +117,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * 256;
@@ -114,7 +132,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc_mma_bf16(d0, make_sdesc(a1 + k * 32, 16, 1024), make_sdesc(b1 + k * 2048, 8192, 1024), id1, acc_on);
             tc_mma_bf16(d0 + 64, make_sdesc(a2 + k * 32, 16, 1024), make_sdesc(b2 + k * 32, 16, 1024), id2, acc_on);
           }
-          tc_commit(&empty[stage]);
+          if (CL > 1)
+            tc_commit_mc(&empty[stage], kMask);  // the stage holds the peer's multicast operand too
+          else
+            tc_commit(&empty[stage]);
           if (++stage == DU_STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[acc]);
@@ -126,8 +147,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint8_t* stg = sE + ew * TC_STAGE_OUT;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int mt = t % p.tiles_m, nt = t / p.tiles_m;
+    for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
+      const int mt = t % p.tiles_m, nt = (t / p.tiles_m) * CL + crank;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int r0 = mt * TC_BM + quad * 32;
@@ -139,7 +160,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // TMEM drained into registers: release it to the MMA early
       const int n0 = nt * DU_NP + half * 32;
+#ifdef MECEFO_DBG_DUAL_NOEPI
+      if (false) {
+#else
       if (n0 < p.NP) {
+#endif
         // g <- sigmoid(gate) in place; u <- silu(gate)*... reuse registers to stay spill-free
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -151,9 +176,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           u[j] = du;
           d[j] = act;
         }
+#ifdef MECEFO_DBG_DUAL_NOSTORE
+        if (d[0] == 1234.5f && g[3] == 77.f && u[5] == 1.f) stg[lane] = 1;  // keep the math alive
+        if (false) {
+#else
+        {
+#endif
         if (p.has_act) stage_store32(stg, &tmAct, d, PREC_BF16, 0, n0, r0, lane);
         stage_store32(stg, &tmDg, g, PREC_BF16, 0, n0, r0, lane);
         stage_store32(stg, &tmDu, u, PREC_BF16, 0, n0, r0, lane);
+        }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -162,6 +194,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");

@@ -62,12 +62,15 @@ def test_exact_backward_hd64(cuda, prec, tol, T, seqs):
         assert R.rel_err(g[k].cpu().numpy(), g_ref[k]) < tol, k
 
 
-def test_lean_backward_hd64_lowrank_r128(cuda):
-    cfg, d, W, x, dy = _setup(seqs=2)
+@pytest.mark.parametrize("seqs", [2, 16])
+def test_lean_backward_hd64_lowrank_r128(cuda, seqs):
+    """seqs=16 (4096 tokens) runs the fused recompute kernel in its 2-CTA
+    cluster form (token operands multicast across column-tile pairs)."""
+    cfg, d, W, x, dy = _setup(seqs=seqs)
     rng = np.random.Generator(np.random.PCG64(9))
     basis = {k: np.linalg.qr(rng.normal(size=(n, 128)))[0] for k, n in (("gate", 512), ("up", 512), ("down", 1376))}
-    _, lean_ref = R.block_fwd(d, W, 0, x.reshape(2, 256, -1), lean=True)
-    dx_ref, g_ref = R.block_bwd_neighbor(d, W, 0, lean_ref, dy.reshape(2, 256, -1), basis)
+    _, lean_ref = R.block_fwd(d, W, 0, x.reshape(seqs, 256, -1), lean=True)
+    dx_ref, g_ref = R.block_bwd_neighbor(d, W, 0, lean_ref, dy.reshape(seqs, 256, -1), basis)
     w = mdl.init_weights(cfg, 0, precision="bf16")
     _, cache = mdl.forward_block(cfg, w.layers[0], torch.tensor(x, dtype=torch.float32, device="cuda"),
                                  mdl.CACHE_FFN_INPUT_ONLY)
