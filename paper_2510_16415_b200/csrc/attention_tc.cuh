@@ -5,9 +5,11 @@
 // of TMEM), the softmax is exact and single-pass — no online rescaling:
 //   1. TMA: Q block (128x64), K and V rows [0, nk) (nk <= 256) -> smem (SW128)
 //   2. tcgen05.mma  S = Q K^T            -> TMEM cols [0, nk)
-//   3. 4 warps (one query row per thread): row max, p = exp(scale (s - max)),
-//      causal mask, row sum; P (bf16) -> smem in the UMMA K-major SW128 layout
-//   4. tcgen05.mma  O = P V (V as an MN-major B operand) -> TMEM cols [256,320)
+//   3. 8 warps, two per TMEM lane quadrant (one query row per thread, each
+//      warp of a pair owns half of the key columns; partial max / sum meet in
+//      smem): row max, p = exp(scale (s - max)), causal mask, row sum; P
+//      (bf16) -> smem in the UMMA K-major SW128 layout
+//   4. tcgen05.mma  O = P V (V as an MN-major B operand) -> TMEM cols [0,64)
 //   5. O / rowsum -> ctx (bf16), LSE (full cache only)
 // q/k arrive RoPE-rotated from the QKV GEMM epilogue (model.py:281-288,
 // 323-331). The (B,H,T,T) probabilities never touch HBM.
@@ -24,18 +26,21 @@ struct AttnTcArgs {
   float scale;
 };
 
-constexpr int ATC_THREADS = 128;
-constexpr int ATC_SMEM = 16384 + 32768 + 32768 + 65536 + 1024 + 256;
+constexpr int ATC_THREADS = 256;
+// smem: [Q 16 KB][K 32 KB][pad 16 KB][V 32 KB] + barriers/reductions. P (up to
+// 64 KB) overwrites Q|K|pad once S = Q K^T has completed, so two CTAs fit
+// per SM (TMEM: 256 columns each; O reuses S's first 64 columns).
+constexpr int ATC_SMEM = 16384 + 32768 + 16384 + 32768 + 1024 + 256 + 2048;
 
-__global__ void __launch_bounds__(ATC_THREADS, 1)
+__global__ void __launch_bounds__(ATC_THREADS, 2)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, AttnTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + 16384;
-  uint8_t* sV = sK + 32768;
-  uint8_t* sP = sV + 32768;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 65536);
+  uint8_t* sV = sK + 32768 + 16384;
+  uint8_t* sP = smem;  // aliases Q|K|pad after the S MMA
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 32768);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -51,7 +56,7 @@ __global__ void __launch_bounds__(ATC_THREADS, 1)
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(512u)
+                 "r"(256u)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -82,27 +87,38 @@ __global__ void __launch_bounds__(ATC_THREADS, 1)
   mbar_wait(&bars[1], 0);
   tc_fence_after();
 
-  const int row = warp * 32 + lane;
+  const int quad = warp & 3, hf = warp >> 2;  // TMEM lane quadrant, key-column half
+  const int row = quad * 32 + lane;
   const int qi = q0 + row;  // query position in the sequence
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16);
   const float c2 = a.scale * 1.4426950408889634f;
+  const int hw = nk >> 1;          // key columns per half (64 or 128)
+  const int cb = hf * hw;          // first key column of this half
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [2][128] max, then [2][128] sum
   float mx = -INFINITY;
-  for (int c = 0; c < nk / 16; ++c) {
-    float v[16];
-    tmem_ld16(taddr + c * 16, v);
+  for (int cc = 0; cc < hw; cc += 32) {
+    float v[32];
+    tmem_ld16_nowait(taddr + cb + cc, v);
+    tmem_ld16_nowait(taddr + cb + cc + 16, v + 16);
+    tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (c * 16 + j <= qi) mx = fmaxf(mx, v[j]);
+    for (int j = 0; j < 32; ++j)
+      if (cb + cc + j <= qi) mx = fmaxf(mx, v[j]);
   }
+  red[hf * 128 + row] = mx;
+  __syncthreads();
+  mx = fmaxf(red[row], red[128 + row]);
   const bool valid = row < nq;
   float l = 0.f;
-  for (int c = 0; c < nk / 16; ++c) {
-    float v[16];
-    tmem_ld16(taddr + c * 16, v);
-    uint32_t pk[8];
+  for (int cc = 0; cc < hw; cc += 32) {
+    float v[32];
+    tmem_ld16_nowait(taddr + cb + cc, v);
+    tmem_ld16_nowait(taddr + cb + cc + 16, v + 16);
+    tmem_wait_ld();
+    uint32_t pk[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k0 = c * 16 + 2 * j;
+    for (int j = 0; j < 16; ++j) {
+      const int k0 = cb + cc + 2 * j;
       const float p0 = (valid && k0 <= qi) ? exp2f((v[2 * j] - mx) * c2) : 0.f;
       const float p1 = (valid && k0 + 1 <= qi) ? exp2f((v[2 * j + 1] - mx) * c2) : 0.f;
       __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
@@ -111,50 +127,55 @@ __global__ void __launch_bounds__(ATC_THREADS, 1)
       l += back.x + back.y;
       pk[j] = *reinterpret_cast<uint32_t*>(&hp);
     }
-    // P row `row`, keys [16c, 16c+16): 64-key block c/4, bytes (c%4)*32 .. +32 of the 128-B row
-    uint8_t* blk = sP + (c >> 2) * 16384 + row * 128;
-    const int u0 = (c & 3) * 2;
-    *reinterpret_cast<uint4*>(blk + (((u0) ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    *reinterpret_cast<uint4*>(blk + (((u0 + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    // P row `row`, keys [cb+cc, cb+cc+32): 64-key block, 16-byte units u0..u0+3 of the 128-B row
+    const int kk = cb + cc;
+    uint8_t* blk = sP + (kk >> 6) * 16384 + row * 128;
+    const int u0 = (kk & 63) >> 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(blk + (((u0 + q) ^ (row & 7)) << 4)) =
+          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
   }
+  red[256 + hf * 128 + row] = l;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
+  l = red[256 + row] + red[384 + row];
   if (threadIdx.x == 0) {
     tc_fence_after();
     // O = P V: A = P K-major (K = keys), B = V MN-major (N = d = 64)
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
     for (int s = 0; s < nk / 16; ++s)
-      tc_mma_bf16(tmem + 256, make_sdesc(smem_u32(sP) + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
+      tc_mma_bf16(tmem, make_sdesc(smem_u32(sP) + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
                   make_sdesc(smem_u32(sV) + s * 2048, 8192, 1024), idesc, s > 0 ? 1u : 0u);
     tc_commit(&bars[2]);
   }
   mbar_wait(&bars[2], 0);
   tc_fence_after();
   const float il = 1.f / l;
-  uint32_t ow[32];
+  // this half's 32 output columns [hf*32, hf*32+32)
+  float ov[32];
+  tmem_ld16_nowait(taddr + hf * 32, ov);
+  tmem_ld16_nowait(taddr + hf * 32 + 16, ov + 16);
+  tmem_wait_ld();
+  uint32_t ow[16];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float v[16];
-    tmem_ld16(taddr + 256 + c * 16, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      __nv_bfloat162 hp = __floats2bfloat162_rn(v[2 * j] * il, v[2 * j + 1] * il);
-      ow[c * 8 + j] = *reinterpret_cast<uint32_t*>(&hp);
-    }
+  for (int j = 0; j < 16; ++j) {
+    __nv_bfloat162 hp = __floats2bfloat162_rn(ov[2 * j] * il, ov[2 * j + 1] * il);
+    ow[j] = *reinterpret_cast<uint32_t*>(&hp);
   }
   if (valid) {
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.ctx) + (int64_t)(row0 + qi) * a.ld_ctx +
-                                          h * 64);
+                                          h * 64 + hf * 32);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dst[u] = make_uint4(ow[4 * u], ow[4 * u + 1], ow[4 * u + 2], ow[4 * u + 3]);
-    if (a.lse) a.lse[(int64_t)(row0 + qi) * a.H + h] = mx * a.scale + logf(l);
+    for (int u = 0; u < 4; ++u) dst[u] = make_uint4(ow[4 * u], ow[4 * u + 1], ow[4 * u + 2], ow[4 * u + 3]);
+    if (a.lse && hf == 0) a.lse[(int64_t)(row0 + qi) * a.H + h] = mx * a.scale + logf(l);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u) : "memory");
   }
 }
 
