@@ -318,11 +318,17 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     outs.prec[k] = slots[k].prec;
     outs.reduce[k] = slots[k].reduce;
   }
+  CUtensorMap tr;  // fp32 residual boxes (same 32x32 SW128 layout as the fp32 store)
+  std::memset(&tr, 0, sizeof(tr));
+  if (ep.kind == EPI_STORE && ep.residual && outs.used[0] && outs.prec[0] == PREC_F32 && !g.paired)
+    TRY(make_tmap(e, &tr, ep.residual, g.N, g.M, ep.ldr, 32, 32, 1, 128));
   {  // timing experiments only: MECEFO_DBG_NOEPI drops every output, MECEFO_DBG_NOROPE the rotation
     static const bool no_epi = getenv("MECEFO_DBG_NOEPI") != nullptr;
     static const bool no_rope = getenv("MECEFO_DBG_NOROPE") != nullptr;
     if (no_epi) outs.used[0] = outs.used[1] = outs.used[2] = 0;
     if (no_rope) p.epi.rope_cos = nullptr;
+    static const bool no_res = getenv("MECEFO_DBG_NORES") != nullptr;
+    if (no_res) p.epi.residual = nullptr;
   }
   auto kern = gemm_tc_kernel<BN, AK, BKM, CL>;
   static bool attr_set = false;
@@ -332,7 +338,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   }
   const int grid = CL * std::min(p.num_tiles_cl, kNumSMs / CL);
   if (CL == 1) {
-    CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, ta, tb, to[0], to[1], to[2], p, outs));
+    CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, ta, tb, to[0], to[1], to[2], tr, p, outs));
     return check_launch("gemm_tc_kernel");
   }
   cudaLaunchConfig_t cfg{};
@@ -349,7 +355,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to[0], to[1], to[2], p, outs));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to[0], to[1], to[2], tr, p, outs));
   return check_launch("gemm_tc_kernel<cluster>");
 }
 

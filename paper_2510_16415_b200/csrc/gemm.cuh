@@ -458,7 +458,7 @@ __device__ __forceinline__ void stage_store32_db(uint8_t* stg, int& sb, const CU
 // Epilogue math for output slot `slot` on 16 consecutive output columns n0..
 // of row r (tcgen05 path): 0 = out / act, 1 = gate or d_gate, 2 = up or d_up.
 __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, int n0, int cnt, bool row_ok,
-                                           const float* g, const float* u, float* o) {
+                                           const float* g, const float* u, float* o, bool res_in_smem = false) {
   if (e.kind == EPI_STORE || e.kind == EPI_ATOMIC) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) o[j] = g[j] * e.alpha;
@@ -500,7 +500,7 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
         }
       }
     }
-    if (e.residual && row_ok && cnt > 0) {
+    if (e.residual && !res_in_smem && row_ok && cnt > 0) {
       float t[16];
       load16(e.residual, (int64_t)r * e.ldr + n0, t, min(cnt, 16), PREC_F32);
 #pragma unroll
@@ -546,7 +546,8 @@ template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
-                   const __grid_constant__ CUtensorMap tmO2, GemmDev p, TcOut outs) {
+                   const __grid_constant__ CUtensorMap tmO2, const __grid_constant__ CUtensorMap tmR, GemmDev p,
+                   TcOut outs) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_holder + 2);  // per-epilogue-warp residual-box barriers
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -571,6 +573,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 32 * TC_EPI_WARPS);
     }
+    for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -689,6 +692,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int quad = ew & 3;        // TMEM lane quadrant == warp % 4
     const int half = ew >> 2;       // which half of the column chunks
     uint8_t* stg = sE + ew * TC_STAGE_OUT;
+    // fp32 residual (x + f(x) epilogues): the 32x32 residual box is TMA-loaded
+    // into the staging box (same SW128 layout as the fp32 store), added in
+    // place, and stored — no per-lane strided global reads in the epilogue
+    const bool res_tma = p.epi.kind == EPI_STORE && p.epi.residual != nullptr && outs.used[0] &&
+                         outs.prec[0] == PREC_F32 && !p.paired;
+    uint32_t rphase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int NCHUNK_PLAIN = BN / 32;
@@ -709,6 +718,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int c = half; c < nchunks; c += 2) {
         const int n0 = cbase + c * 32;
         if (n0 >= p.N) continue;  // warp-uniform
+        if (res_tma) {
+          stage_wait(lane);  // the previous store has read the box
+          if (lane == 0) {
+            mbar_expect_tx(&rbar[ew], 32 * 32 * 4);
+            tma_load_2d(stg, &tmR, &rbar[ew], n0, r0);
+          }
+        }
         // all TMEM columns of the chunk in flight before one wait::ld
         float g[32], u[32];
         tmem_ld16_nowait(taddr + c * 32, g);
@@ -728,12 +744,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int slot = 0; slot < 3; ++slot) {  // unrolled: outs.* indexed statically (no local-memory copy)
           if (!outs.used[slot]) continue;
-          stage_wait(lane);
+          const bool rs = slot == 0 && res_tma;
+          if (rs) {
+            mbar_wait(&rbar[ew], rphase);
+            rphase ^= 1;
+          } else {
+            stage_wait(lane);
+          }
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             float o[16];
             const int n0h = n0 + hh * 16;
-            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g + hh * 16, u + hh * 16, o);
+            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g + hh * 16, u + hh * 16, o, rs);
+            if (rs) {  // + residual from the staging box (this lane's row, 16 columns)
+              const uint8_t* rrow = stg + lane * 128;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 r4 = *reinterpret_cast<const float4*>(rrow + (((hh * 4 + q) ^ (lane & 7)) << 4));
+                o[4 * q] += r4.x; o[4 * q + 1] += r4.y; o[4 * q + 2] += r4.z; o[4 * q + 3] += r4.w;
+              }
+            }
             stage_write16(stg, o, outs.prec[slot], hh, lane);
           }
           stage_commit(stg, slot == 0 ? &tmO0 : (slot == 1 ? &tmO1 : &tmO2), outs.reduce[slot], n0, r0, lane);
