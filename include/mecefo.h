@@ -240,6 +240,44 @@ int mecefo_gemm(mecefo_engine* e, int64_t M, int64_t N, int64_t K, const void* a
                 const void* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha, float beta,
                 void* stream);
 
+/* FFN intermediates of a lean block kept for its deferred weight gradients
+ * (approx.py:125-126 binds the low-rank wgrad inside ffn_backward; running it
+ * later for all lean layers at once changes no arithmetic). Caller buffers,
+ * compute precision, tokens rows. */
+typedef struct mecefo_ffn_saved {
+  void* h2;    /* (tokens, hidden): RMSNorm(x1), model.py:213 */
+  void* act;   /* (tokens, ffn): silu(gate) * up, model.py:216 */
+  void* dcat;  /* (tokens, 2 ffn): [d_gate | d_up], model.py:251-253 */
+} mecefo_ffn_saved;
+
+/* approx.py:99-134 backward_block_neighbor WITHOUT the FFN weight gradients:
+ * dx, the norm_ffn grad (gr->norm_ffn, gr->alpha_ffn) and the intermediates in
+ * `saved`; dy_c (compute precision) must stay alive until
+ * mecefo_lowrank_wgrads_batched consumed it. */
+int mecefo_backward_block_neighbor_main(mecefo_engine* e, const mecefo_layer_weights* lw,
+                                        const mecefo_block_cache* c, const float* dy, const void* dy_c, float* dx,
+                                        void* dx_c, const mecefo_layer_grads* gr, const mecefo_ffn_saved* saved,
+                                        int64_t tokens, void* workspace, size_t workspace_bytes, void* stream);
+
+/* One lean block's deferred low-rank FFN weight gradients (approx.py:24-42 for
+ * gate, up and down; model.py:247, 255-256): grad += alpha * d2^T (inp V1) V1^T. */
+typedef struct mecefo_lowrank_job {
+  const void* dy_c;               /* (tokens, hidden) compute precision */
+  mecefo_ffn_saved saved;
+  const mecefo_projection* proj;
+  float* grad_gu;                 /* (2 ffn, hidden) fp32 [gate; up] grads, accumulated */
+  float* grad_down;               /* (hidden, ffn) fp32, accumulated */
+  float alpha;                    /* Eq. (1) weight of the FFN kinds */
+} mecefo_lowrank_job;
+
+/* All jobs (HOST array) in as few launches as possible: bf16 with a rank_pad
+ * multiple of 128 runs each product of up to 8 blocks as ONE grouped tcgen05
+ * launch; otherwise one chain per job. */
+size_t mecefo_lowrank_batched_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t rank_pad,
+                                             int32_t count);
+int mecefo_lowrank_wgrads_batched(mecefo_engine* e, const mecefo_lowrank_job* jobs, int32_t count, int64_t tokens,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
 /* One matrix of a batched projection refresh (approx.py:66-87 refreshes
  * every (layer, kind) basis of a rank at once; each is linalg.py:97-142). */
 typedef struct mecefo_subspace_job {

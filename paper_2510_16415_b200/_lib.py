@@ -120,6 +120,21 @@ class SubspaceJob(ctypes.Structure):
     ]
 
 
+class FfnSaved(ctypes.Structure):
+    _fields_ = [("h2", c_void_p), ("act", c_void_p), ("dcat", c_void_p)]
+
+
+class LowrankJob(ctypes.Structure):
+    _fields_ = [
+        ("dy_c", c_void_p),
+        ("saved", FfnSaved),
+        ("proj", POINTER(Projection)),
+        ("grad_gu", c_void_p),
+        ("grad_down", c_void_p),
+        ("alpha", c_float),
+    ]
+
+
 # name -> (restype, argtypes)
 _SIGNATURES = {
     "mecefo_last_error": (c_char_p, []),
@@ -195,6 +210,13 @@ _SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int32, c_void_p,
          c_int64, c_float, c_float, c_void_p],
     ),
+    "mecefo_backward_block_neighbor_main": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+         c_size_t, c_void_p],
+    ),
+    "mecefo_lowrank_batched_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32, c_int32]),
+    "mecefo_lowrank_wgrads_batched": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_size_t, c_void_p]),
     "mecefo_subspace_workspace_bytes": (c_size_t, [c_void_p, c_int32]),
     "mecefo_subspace_iteration_batched": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_size_t, c_void_p]),
 }

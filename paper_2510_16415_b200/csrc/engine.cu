@@ -245,7 +245,14 @@ struct GemmCall {
   // block-diagonal batching: M tile mt reads B columns shifted by mt * b_diag_off
   // (two independent products sharing one launch; needs 128-row blocks)
   int64_t b_diag_off = 0;
+  // grouped launch: `groups` products of this shape, operand/output base
+  // pointers per group (ga/gb/go override a.p/b.p/epi.out); same strides
+  int groups = 1;
+  const void* ga[8] = {};
+  const void* gb[8] = {};
+  void* go[8] = {};
 };
+constexpr int kMaxGroups = 8;
 
 Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, float beta = 0.f,
                    const float* residual = nullptr, int64_t ldr = 0) {
@@ -256,15 +263,23 @@ Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, floa
   return e;
 }
 
-template <int BN, bool AK, bool BKM, int CL>
+template <int BN, bool AK, bool BKM, int CL, int NG>
 int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   using C = TcCfg<BN>;
-  CUtensorMap ta, tb;
-  if (AK) TRY(make_tmap(e, &ta, g.a.p, g.K, g.M, g.a.ld, 64, TC_BM));
-  else TRY(make_tmap(e, &ta, g.a.p, g.M, g.K, g.a.ld, 64, 64));
+  static_assert(NG == 1 || CL == 1, "grouped launches are single-CTA");
+  const int ng = NG > 1 ? g.groups : 1;
+  if (ng < 1 || ng > NG) return set_err(MECEFO_ERR_CONSISTENCY, "group count %d outside [1, %d]", ng, NG);
+  TcMaps<NG> mp;
+  std::memset(&mp, 0, sizeof(mp));
   const int64_t rowsB = g.paired ? g.pair_off + g.N : g.N + g.b_diag_off * ((g.M + TC_BM - 1) / TC_BM - 1);
-  if (BKM) TRY(make_tmap(e, &tb, g.b.p, g.K, rowsB, g.b.ld, 64, (g.paired || CL > 1) ? BN / 2 : BN));
-  else TRY(make_tmap(e, &tb, g.b.p, rowsB, g.K, g.b.ld, 64, 64));
+  for (int q = 0; q < ng; ++q) {
+    const void* pa = NG > 1 ? g.ga[q] : g.a.p;
+    const void* pb = NG > 1 ? g.gb[q] : g.b.p;
+    if (AK) TRY(make_tmap(e, &mp.a[q], pa, g.K, g.M, g.a.ld, 64, TC_BM));
+    else TRY(make_tmap(e, &mp.a[q], pa, g.M, g.K, g.a.ld, 64, 64));
+    if (BKM) TRY(make_tmap(e, &mp.b[q], pb, g.K, rowsB, g.b.ld, 64, (g.paired || CL > 1) ? BN / 2 : BN));
+    else TRY(make_tmap(e, &mp.b[q], pb, rowsB, g.K, g.b.ld, 64, 64));
+  }
   GemmDev p{};
   p.M = (int)g.M; p.N = (int)g.N; p.K = (int)g.K;
   p.paired = g.paired ? 1 : 0;
@@ -277,14 +292,13 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   p.tiles_m = (int)((g.M + TC_BM - 1) / TC_BM);
   const int cols_per_tile = g.paired ? BN / 2 : BN;
   p.tiles_n = (int)((g.N + cols_per_tile - 1) / cols_per_tile);
-  p.num_tiles = p.tiles_m * p.tiles_n * p.split;
+  p.num_tiles = p.tiles_m * p.tiles_n * p.split * ng;
   p.tiles_m_cl = (p.tiles_m + CL - 1) / CL;
-  p.num_tiles_cl = p.tiles_m_cl * p.tiles_n * p.split;
+  p.split_tiles = p.tiles_m_cl * p.tiles_n * p.split;
+  p.num_tiles_cl = p.split_tiles * ng;
   p.epi = g.epi;
   // output slots -> TMA store / reduce-add maps (32 x 32 boxes, swizzled)
   TcOut outs{};
-  CUtensorMap to[3];
-  std::memset(to, 0, sizeof(to));
   const Epilogue& ep = g.epi;
   struct Slot { void* ptr; int64_t ld; int prec; int reduce; };
   Slot slots[3] = {{nullptr, 0, 0, 0}, {nullptr, 0, 0, 0}, {nullptr, 0, 0, 0}};
@@ -310,18 +324,22 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     default:
       return set_err(MECEFO_ERR_CONSISTENCY, "unknown epilogue kind %d", ep.kind);
   }
+  if (NG > 1 && (slots[1].ptr || slots[2].ptr || ep.residual || ep.rope_cos))
+    return set_err(MECEFO_ERR_CONSISTENCY, "grouped launches support plain store / accumulate epilogues only");
   for (int k = 0; k < 3; ++k) {
     if (!slots[k].ptr) continue;
     const int f32 = slots[k].prec == PREC_F32 ? 1 : 0;
-    TRY(make_tmap(e, &to[k], slots[k].ptr, g.N, g.M, slots[k].ld, 32, 32, f32, f32 ? 128 : 64));
+    CUtensorMap* dst = k == 0 ? &mp.o0[0] : (k == 1 ? &mp.o1 : &mp.o2);
+    for (int q = 0; q < (k == 0 ? ng : 1); ++q)
+      TRY(make_tmap(e, dst + q, (k == 0 && NG > 1) ? g.go[q] : slots[k].ptr, g.N, g.M, slots[k].ld, 32, 32, f32,
+                    f32 ? 128 : 64));
     outs.used[k] = 1;
     outs.prec[k] = slots[k].prec;
     outs.reduce[k] = slots[k].reduce;
   }
-  CUtensorMap tr;  // fp32 residual boxes (same 32x32 SW128 layout as the fp32 store)
-  std::memset(&tr, 0, sizeof(tr));
+  // fp32 residual boxes (same 32x32 SW128 layout as the fp32 store)
   if (ep.kind == EPI_STORE && ep.residual && outs.used[0] && outs.prec[0] == PREC_F32 && !g.paired)
-    TRY(make_tmap(e, &tr, ep.residual, g.N, g.M, ep.ldr, 32, 32, 1, 128));
+    TRY(make_tmap(e, &mp.r, ep.residual, g.N, g.M, ep.ldr, 32, 32, 1, 128));
   {  // timing experiments only: MECEFO_DBG_NOEPI drops every output, MECEFO_DBG_NOROPE the rotation
     static const bool no_epi = getenv("MECEFO_DBG_NOEPI") != nullptr;
     static const bool no_rope = getenv("MECEFO_DBG_NOROPE") != nullptr;
@@ -330,7 +348,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     static const bool no_res = getenv("MECEFO_DBG_NORES") != nullptr;
     if (no_res) p.epi.residual = nullptr;
   }
-  auto kern = gemm_tc_kernel<BN, AK, BKM, CL>;
+  auto kern = gemm_tc_kernel<BN, AK, BKM, CL, NG>;
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -338,7 +356,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   }
   const int grid = CL * std::min(p.num_tiles_cl, kNumSMs / CL);
   if (CL == 1) {
-    CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, ta, tb, to[0], to[1], to[2], tr, p, outs));
+    CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, mp, p, outs));
     return check_launch("gemm_tc_kernel");
   }
   cudaLaunchConfig_t cfg{};
@@ -355,16 +373,16 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to[0], to[1], to[2], tr, p, outs));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mp, p, outs));
   return check_launch("gemm_tc_kernel<cluster>");
 }
 
-template <int BN, int CL>
+template <int BN, int CL, int NG = 1>
 int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
-  if (g.a.km && g.b.km) return launch_tc<BN, true, true, CL>(e, g, s);
-  if (g.a.km && !g.b.km) return launch_tc<BN, true, false, CL>(e, g, s);
-  if (!g.a.km && g.b.km) return launch_tc<BN, false, true, CL>(e, g, s);
-  return launch_tc<BN, false, false, CL>(e, g, s);
+  if (g.a.km && g.b.km) return launch_tc<BN, true, true, CL, NG>(e, g, s);
+  if (g.a.km && !g.b.km) return launch_tc<BN, true, false, CL, NG>(e, g, s);
+  if (!g.a.km && g.b.km) return launch_tc<BN, false, true, CL, NG>(e, g, s);
+  return launch_tc<BN, false, false, CL, NG>(e, g, s);
 }
 
 // TMA-multicast CTA pairs along M whenever there are at least two M tiles
@@ -392,7 +410,7 @@ int choose_bn(const GemmCall& g) {
   for (int BN : {256, 128, 64}) {
     if (BN > 64 && nacc <= BN / 2) continue;
     const int64_t cpt = g.paired ? BN / 2 : BN;
-    const int64_t tiles = tm * ((g.N + cpt - 1) / cpt);
+    const int64_t tiles = tm * ((g.N + cpt - 1) / cpt) * std::max(1, g.groups);
     const double eff = BN == 256 ? 1.0 : (BN == 128 ? 1.15 : 1.35);
     const double cost = (double)((tiles + kNumSMs - 1) / kNumSMs) * BN * eff;
     if (cost < best_cost * 0.999) { best_cost = cost; best = BN; }
@@ -404,7 +422,7 @@ int tiles_for(const GemmCall& g, int prec) {
   if (prec == PREC_BF16) {
     const int BN = choose_bn(g);
     const int64_t cpt = g.paired ? BN / 2 : BN;
-    return (int)(((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt));
+    return (int)(((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt)) * std::max(1, g.groups);
   }
   const int64_t cpt = g.paired ? 32 : 64;
   return (int)(((g.M + 63) / 64) * ((g.N + cpt - 1) / cpt));
@@ -415,12 +433,21 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   const double ncols = (double)(g.paired ? 2 * g.N : g.N);
   const double out_bytes = g.epi.kind == EPI_STORE ? (g.epi.out_prec == PREC_BF16 ? 2.0 : 4.0) * (1 + (g.epi.beta != 0.f) + (g.epi.residual != nullptr))
                          : (g.epi.kind == EPI_ATOMIC ? 8.0 : 3.0 * e->ps);
-  ProfScope prof(g.tag, 2.0 * g.M * ncols * g.K,
-                 (double)e->ps * ((double)g.M * g.K + ncols * g.K) + out_bytes * (double)g.M * (double)g.N, s);
+  const double ngr = (double)std::max(1, g.groups);
+  ProfScope prof(g.tag, 2.0 * g.M * ncols * g.K * ngr,
+                 ngr * ((double)e->ps * ((double)g.M * g.K + ncols * g.K) + out_bytes * (double)g.M * (double)g.N), s);
   if (g.split > 1 && g.epi.kind != EPI_ATOMIC)
     return set_err(MECEFO_ERR_CONSISTENCY, "split-K requires the atomic epilogue");
   if (g.b_diag_off && (e->prec != PREC_BF16 || g.paired))
     return set_err(MECEFO_ERR_CONSISTENCY, "block-diagonal batching is a tcgen05 (bf16), unpaired mode");
+  if (g.groups > 1) {
+    if (e->prec != PREC_BF16 || g.paired || g.groups > kMaxGroups)
+      return set_err(MECEFO_ERR_CONSISTENCY, "grouped GEMM: bf16, unpaired, <= %d groups", kMaxGroups);
+    const int BN = choose_bn(g);
+    if (BN == 256) return dispatch_tc_major<256, 1, kMaxGroups>(e, g, s);
+    if (BN == 128) return dispatch_tc_major<128, 1, kMaxGroups>(e, g, s);
+    return dispatch_tc_major<64, 1, kMaxGroups>(e, g, s);
+  }
   if (e->prec == PREC_BF16) {
     if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
     const int BN = choose_bn(g);
@@ -461,8 +488,16 @@ int gemm_accumulate(mecefo_engine* e, GemmCall g, float* out, int64_t ldo, float
     Epilogue ep{};
     ep.kind = EPI_ATOMIC; ep.out = out; ep.ldo = ldo; ep.alpha = alpha; ep.out_prec = PREC_F32;
     g.epi = ep;
-    // floor: tiles x split must fit ONE wave (148 CTAs), a 149th CTA doubles the time
-    g.split = std::max(1, std::min(kNumSMs / tiles, kblocks / 4));
+    // wave-aware split: maximise units / (waves * 148) (a 149th CTA doubles
+    // the time of a one-wave launch); ties go to the smaller split
+    auto eff = [&](int sp) {
+      const double units = (double)tiles * sp;
+      return units / (std::ceil(units / kNumSMs) * kNumSMs);
+    };
+    int best = 1;
+    for (int sp = 2; sp <= std::min(32, kblocks / 4); ++sp)
+      if (eff(sp) > eff(best) + 0.01) best = sp;
+    g.split = best;
     if (e->prec == PREC_F32) g.split = std::max(1, std::min(g.split * 4, (int)((g.K + 15) / 16) / 8));
   } else {
     g.epi = epi_store(out, ldo, PREC_F32, alpha, 1.f);
@@ -913,7 +948,7 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
       const int64_t n = 2 * rp * 2 * f;
       ProfScope prof("lowrank.cast", 0.0, 6.0 * n / 2, s);
       CUDA_TRY(pdl_launch(cast_blockdiag_t_kernel, dim3((unsigned)std::min<int64_t>((n + 255) / 256, 4 * kNumSMs)),
-                          dim3(256), 0, s, (const float*)QT, (__nv_bfloat16*)QTc, (int)rp, (int)f));
+                          dim3(256), 0, s, (const float*)QT, (__nv_bfloat16*)QTc, (int)rp, (int)f, (int64_t)1));
       TRY(check_launch("cast_blockdiag_t_kernel"));
     }
     g = GemmCall();
@@ -1042,10 +1077,35 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
 
 }  // namespace
 
+static int neighbor_backward_impl(mecefo_engine* e, const mecefo_layer_weights* lw, const mecefo_block_cache* c,
+                                  const float* dy, const void* dy_c, float* dx, void* dx_c,
+                                  const mecefo_layer_grads* gr, const mecefo_projection* pj,
+                                  const mecefo_ffn_saved* saved, int64_t tokens, void* wsp, size_t ws_bytes,
+                                  void* stream);
+
 int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights* lw, const mecefo_block_cache* c,
                                    const float* dy, const void* dy_c, float* dx, void* dx_c,
                                    const mecefo_layer_grads* gr, const mecefo_projection* pj, int64_t tokens, void* wsp,
                                    size_t ws_bytes, void* stream) {
+  return neighbor_backward_impl(e, lw, c, dy, dy_c, dx, dx_c, gr, pj, nullptr, tokens, wsp, ws_bytes, stream);
+}
+
+int mecefo_backward_block_neighbor_main(mecefo_engine* e, const mecefo_layer_weights* lw,
+                                        const mecefo_block_cache* c, const float* dy, const void* dy_c, float* dx,
+                                        void* dx_c, const mecefo_layer_grads* gr, const mecefo_ffn_saved* saved,
+                                        int64_t tokens, void* wsp, size_t ws_bytes, void* stream) {
+  if (!saved || !saved->h2 || !saved->act || !saved->dcat)
+    return set_err(MECEFO_ERR_CONTRACT, "neighbor_main needs caller buffers for h2, act and dcat");
+  if (e && e->prec == PREC_BF16 && !dy_c)
+    return set_err(MECEFO_ERR_CONTRACT, "neighbor_main needs the compute-precision dy (it is kept for the deferred Wgrads)");
+  return neighbor_backward_impl(e, lw, c, dy, dy_c, dx, dx_c, gr, nullptr, saved, tokens, wsp, ws_bytes, stream);
+}
+
+static int neighbor_backward_impl(mecefo_engine* e, const mecefo_layer_weights* lw, const mecefo_block_cache* c,
+                                  const float* dy, const void* dy_c, float* dx, void* dx_c,
+                                  const mecefo_layer_grads* gr, const mecefo_projection* pj,
+                                  const mecefo_ffn_saved* saved, int64_t tokens, void* wsp, size_t ws_bytes,
+                                  void* stream) {
   TRY(check_tokens(e, tokens));
   auto s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t b = tokens, m = e->d.hidden, f = e->d.ffn;
@@ -1063,11 +1123,17 @@ int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights*
   }
   void *h2, *d_act, *act, *dcat;
   float *inv2, *dh;
-  TRY(ws.take(b * m * e->ps, &h2));
+  if (saved) {  // deferred Wgrads: the FFN intermediates go to caller buffers
+    h2 = saved->h2;
+    act = saved->act;
+    dcat = saved->dcat;
+  } else {
+    TRY(ws.take(b * m * e->ps, &h2));
+    TRY(ws.take(b * f * e->ps, &act));
+    TRY(ws.take(b * 2 * f * e->ps, &dcat));
+  }
   TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv2)));
   TRY(ws.take(b * f * e->ps, &d_act));
-  TRY(ws.take(b * f * e->ps, &act));
-  TRY(ws.take(b * 2 * f * e->ps, &dcat));
   TRY(ws.take(b * m * 4, reinterpret_cast<void**>(&dh)));
   // recompute h2 = rmsnorm(x1) (approx.py:128 -> model.py:213)
   TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
@@ -1106,6 +1172,7 @@ int mecefo_backward_block_neighbor(mecefo_engine* e, const mecefo_layer_weights*
   // dx = dy + rmsnorm_bwd(x1, ...)   (model.py:259, approx.py:130)
   TRY(rmsnorm_bwd(e, ws, c->x1, lw->norm_ffn, inv2, dh, dy, dx, dx_c, gr->norm_ffn, gr->alpha_ffn, b, m, s));
   // FFN weight gradients
+  if (saved) return MECEFO_OK;  // deferred: mecefo_lowrank_wgrads_batched
   if (pj) {
     TRY(lowrank_ffn_wgrads(e, ws, pj, dy_c, h2, act, dcat, gr, b, s));
   } else {
@@ -1510,6 +1577,149 @@ SubGemmJob sub_job(const float* a, int64_t lda, bool a_kmajor, const float* b, i
   return j;
 }
 }  // namespace
+
+namespace {
+bool lowrank_grouped_ok(const mecefo_engine* e, const mecefo_lowrank_job* jobs, int count) {
+  if (e->prec != PREC_BF16) return false;
+  const int64_t rp = jobs[0].proj ? jobs[0].proj->rank_pad : 0;
+  if (rp <= 0 || rp % TC_BM != 0) return false;
+  for (int i = 0; i < count; ++i) {
+    const mecefo_projection* pj = jobs[i].proj;
+    if (!pj || pj->rank_pad != rp || !pj->v1_gu || !pj->v1t_gu || !pj->v1[2] || !pj->v1t[2]) return false;
+    if (!jobs[i].grad_gu || !jobs[i].grad_down || !jobs[i].dy_c) return false;
+  }
+  return true;
+}
+size_t lowrank_group_bytes(const mecefo_engine* e, int64_t b, int64_t rp) {
+  const int64_t m = e->d.hidden, f = e->d.ffn, ps = e->ps;
+  auto al = [](int64_t x) { return (size_t)((x + 255) & ~int64_t(255)); };
+  return al(b * 2 * rp * ps) + al(2 * rp * f * 4) + al(2 * rp * 2 * f * ps) + al(rp * m * 4) + al(rp * m * ps);
+}
+}  // namespace
+
+size_t mecefo_lowrank_batched_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t rank_pad,
+                                             int32_t count) {
+  if (!e || tokens < 1 || rank_pad < 1 || count < 1) return 0;
+  const int per = std::min<int>(count, kMaxGroups);
+  // grouped path: per-group scratch for one chunk; fallback: one neighbour chain
+  return std::max(lowrank_group_bytes(e, tokens, rank_pad) * per + 4096,
+                  mecefo_workspace_bytes(e, tokens, rank_pad));
+}
+
+int mecefo_lowrank_wgrads_batched(mecefo_engine* e, const mecefo_lowrank_job* jobs, int32_t count, int64_t tokens,
+                                  void* wsp, size_t ws_bytes, void* stream) {
+  TRY(check_tokens(e, tokens));
+  if (!jobs || count < 0) return set_err(MECEFO_ERR_CONTRACT, "null job list");
+  if (count == 0) return MECEFO_OK;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t b = tokens, m = e->d.hidden, f = e->d.ffn, ps = e->ps;
+  for (int i = 0; i < count; ++i)
+    if (!jobs[i].proj || !jobs[i].saved.h2 || !jobs[i].saved.act || !jobs[i].saved.dcat || !jobs[i].dy_c)
+      return set_err(MECEFO_ERR_CONTRACT, "lowrank job %d: missing projection, dy or saved intermediates", i);
+  if (!lowrank_grouped_ok(e, jobs, count)) {  // general path: one neighbour Wgrad chain per job
+    for (int i = 0; i < count; ++i) {
+      Ws ws(wsp, ws_bytes);
+      mecefo_layer_grads gr{};
+      gr.gu = jobs[i].grad_gu;
+      gr.down = jobs[i].grad_down;
+      gr.alpha_ffn = jobs[i].alpha;
+      TRY(lowrank_ffn_wgrads(e, ws, jobs[i].proj, jobs[i].dy_c, jobs[i].saved.h2, jobs[i].saved.act,
+                             jobs[i].saved.dcat, &gr, b, s));
+    }
+    return MECEFO_OK;
+  }
+  const int64_t rp = jobs[0].proj->rank_pad;
+  // Grouped chain (the transposed low-rank path of lowrank_ffn_wgrads, one
+  // launch per product for up to 8 lean layers): the per-layer products are
+  // too small to fill the GPU alone (88-144 CTAs, 8-22 k-blocks).
+  for (int j0 = 0; j0 < count;) {
+    int n = 1;
+    while (j0 + n < count && n < kMaxGroups && jobs[j0 + n].alpha == jobs[j0].alpha) ++n;
+    const mecefo_lowrank_job* J = jobs + j0;
+    const float alpha = J[0].alpha;
+    Ws ws(wsp, ws_bytes);
+    void* P;
+    float *QT, *QTd;
+    void *QTc, *QTdc;
+    TRY(ws.take(n * b * 2 * rp * ps, &P));
+    TRY(ws.take(n * 2 * rp * f * 4, reinterpret_cast<void**>(&QT)));
+    TRY(ws.take(n * 2 * rp * 2 * f * ps, &QTc));
+    TRY(ws.take(n * rp * m * 4, reinterpret_cast<void**>(&QTd)));
+    TRY(ws.take(n * rp * m * ps, &QTdc));
+    auto Pq = [&](int q) { return reinterpret_cast<uint8_t*>(P) + (size_t)q * b * 2 * rp * ps; };
+    GemmCall g;
+    // [P_g | P_u] = h2 [V1_g | V1_u]
+    g.M = b; g.N = 2 * rp; g.K = m;
+    g.a = {J[0].saved.h2, m, true}; g.b = {J[0].proj->v1t_gu, m, true};
+    g.epi = epi_store(Pq(0), 2 * rp, e->prec);
+    g.groups = n;
+    for (int q = 0; q < n; ++q) { g.ga[q] = J[q].saved.h2; g.gb[q] = J[q].proj->v1t_gu; g.go[q] = Pq(q); }
+    g.tag = "lowrank.P";
+    TRY(run_gemm(e, g, s));
+    // [Q_g^T ; Q_u^T] = [P_g | P_u]^T [d_gate | d_up], block-diagonal
+    CUDA_TRY(cudaMemsetAsync(QT, 0, n * 2 * rp * f * 4, s));
+    g = GemmCall();
+    g.M = 2 * rp; g.N = f; g.K = b;
+    g.a = {Pq(0), 2 * rp, false}; g.b = {J[0].saved.dcat, 2 * f, false};
+    g.b_diag_off = f;
+    g.groups = n;
+    for (int q = 0; q < n; ++q) { g.ga[q] = Pq(q); g.gb[q] = J[q].saved.dcat; g.go[q] = QT + (size_t)q * 2 * rp * f; }
+    g.tag = "lowrank.Q";
+    TRY(gemm_accumulate(e, g, QT, f, 1.f, s));
+    {
+      const int64_t nel = (int64_t)n * 2 * rp * 2 * f;
+      ProfScope prof("lowrank.cast", 0.0, 6.0 * nel / 2, s);
+      CUDA_TRY(pdl_launch(cast_blockdiag_t_kernel, dim3((unsigned)std::min<int64_t>((nel + 255) / 256, 8 * kNumSMs)),
+                          dim3(256), 0, s, (const float*)QT, (__nv_bfloat16*)QTc, (int)rp, (int)f, (int64_t)n));
+      TRY(check_launch("cast_blockdiag_t_kernel"));
+    }
+    // [G_g ; G_u] += alpha blockdiag(Q) [V1_g | V1_u]^T
+    g = GemmCall();
+    g.M = 2 * f; g.N = m; g.K = 2 * rp;
+    g.a = {QTc, 2 * f, false}; g.b = {J[0].proj->v1_gu, 2 * rp, true};
+    g.epi = epi_store(J[0].grad_gu, m, PREC_F32, alpha, 1.f);
+    g.groups = n;
+    for (int q = 0; q < n; ++q) {
+      g.ga[q] = reinterpret_cast<uint8_t*>(QTc) + (size_t)q * 2 * rp * 2 * f * ps;
+      g.gb[q] = J[q].proj->v1_gu;
+      g.go[q] = J[q].grad_gu;
+    }
+    g.tag = "lowrank.up_proj";
+    TRY(run_gemm(e, g, s));
+    // down: P_d = act V1_d (into the P buffers), Q_d^T = P_d^T dy, G_d += alpha Q_d V1_d^T
+    g = GemmCall();
+    g.M = b; g.N = rp; g.K = f;
+    g.a = {J[0].saved.act, f, true}; g.b = {J[0].proj->v1t[2], f, true};
+    g.epi = epi_store(Pq(0), rp, e->prec);
+    g.groups = n;
+    for (int q = 0; q < n; ++q) { g.ga[q] = J[q].saved.act; g.gb[q] = J[q].proj->v1t[2]; g.go[q] = Pq(q); }
+    g.tag = "lowrank.P";
+    TRY(run_gemm(e, g, s));
+    CUDA_TRY(cudaMemsetAsync(QTd, 0, n * rp * m * 4, s));
+    g = GemmCall();
+    g.M = rp; g.N = m; g.K = b;
+    g.a = {Pq(0), rp, false}; g.b = {J[0].dy_c, m, false};
+    g.groups = n;
+    for (int q = 0; q < n; ++q) { g.ga[q] = Pq(q); g.gb[q] = J[q].dy_c; g.go[q] = QTd + (size_t)q * rp * m; }
+    g.tag = "lowrank.Q";
+    TRY(gemm_accumulate(e, g, QTd, m, 1.f, s));
+    TRY(cast_to_compute(e, QTd, QTdc, n * rp * m, s));
+    g = GemmCall();
+    g.M = m; g.N = f; g.K = rp;
+    g.a = {QTdc, m, false}; g.b = {J[0].proj->v1[2], rp, true};
+    g.epi = epi_store(J[0].grad_down, f, PREC_F32, alpha, 1.f);
+    g.groups = n;
+    for (int q = 0; q < n; ++q) {
+      g.ga[q] = reinterpret_cast<uint8_t*>(QTdc) + (size_t)q * rp * m * ps;
+      g.gb[q] = J[q].proj->v1[2];
+      g.go[q] = J[q].grad_down;
+    }
+    g.tag = "lowrank.up_proj";
+    TRY(run_gemm(e, g, s));
+    j0 += n;
+  }
+  return MECEFO_OK;
+}
 
 size_t mecefo_subspace_workspace_bytes(const mecefo_subspace_job* jobs, int32_t count) {
   if (!jobs || count < 1) return 0;

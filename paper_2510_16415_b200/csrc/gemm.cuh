@@ -61,8 +61,22 @@ struct GemmDev {
   int kb_per_split;      // k-blocks (of 64) per split
   int kblocks;           // total k-blocks
   int tiles_m, tiles_n, num_tiles;
-  int tiles_m_cl, num_tiles_cl;  // tiles in units of CTA clusters along M (CL = 1 or 2)
+  int tiles_m_cl, num_tiles_cl;  // tiles in units of CTA clusters along M (CL = 1 or 2); x groups
+  int split_tiles;               // tiles_m_cl * tiles_n * split (one group)
   Epilogue epi;
+};
+
+// Tensor maps of one launch. NG > 1: a grouped launch — NG independent
+// products of identical shape (e.g. the same low-rank contraction of every
+// lean layer), each with its own A, B and slot-0 output; the tile index
+// decodes to (group, tile).
+template <int NG>
+struct alignas(64) TcMaps {
+  CUtensorMap a[NG];
+  CUtensorMap b[NG];
+  CUtensorMap o0[NG];
+  CUtensorMap o1, o2;  // paired SwiGLU outputs (NG == 1 only)
+  CUtensorMap r;       // fp32 residual boxes (NG == 1 only)
 };
 
 // ---------------------------------------------------------------------------
@@ -223,9 +237,11 @@ __device__ __forceinline__ void decode_tile(const GemmDev& p, int t, int& mt, in
   nt = rest % p.tiles_n;
   ks = rest / p.tiles_n;
 }
-// Cluster tile t (pairs of M tiles sharing one B tile) -> this CTA's tile.
+// Cluster tile t (pairs of M tiles sharing one B tile) -> this CTA's tile and group.
 __device__ __forceinline__ void decode_tile_cl(const GemmDev& p, int t, int crank, int cl, int& mt, int& nt,
-                                               int& ks) {
+                                               int& ks, int& grp) {
+  grp = t / p.split_tiles;
+  t -= grp * p.split_tiles;
   const int mp = t % p.tiles_m_cl;
   int rest = t / p.tiles_m_cl;
   nt = rest % p.tiles_n;
@@ -542,12 +558,9 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
     o[j] = slot == 2 ? d[j] * silu_f(g[j]) : (d[j] * u[j]) * silu_grad_f(g[j]);
 }
 
-template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL>
+template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL, int NG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
-                   const __grid_constant__ CUtensorMap tmO2, const __grid_constant__ CUtensorMap tmR, GemmDev p,
-                   TcOut outs) {
+    gemm_tc_kernel(const __grid_constant__ TcMaps<NG> mp, GemmDev p, TcOut outs) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -575,8 +588,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.a[0])) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.b[0])) : "memory");
   }
   const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   const int cl_id = blockIdx.x / CL, n_cl = gridDim.x / CL;
@@ -600,8 +613,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
-        int mt, nt, ks;
-        decode_tile_cl(p, t, crank, CL, mt, nt, ks);
+        int mt, nt, ks, grp;
+        decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
+        const CUtensorMap* tmA = &mp.a[NG > 1 ? grp : 0];
+        const CUtensorMap* tmB = &mp.b[NG > 1 ? grp : 0];
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -611,21 +626,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* b = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
           if (A_KMAJOR) {
-            tma_load_2d(a, &tmA, &full[stage], k0, mt * TC_BM);
+            tma_load_2d(a, tmA, &full[stage], k0, mt * TC_BM);
           } else {
-            tma_load_2d(a, &tmA, &full[stage], mt * TC_BM, k0);
-            tma_load_2d(a + 8192, &tmA, &full[stage], mt * TC_BM + 64, k0);
+            tma_load_2d(a, tmA, &full[stage], mt * TC_BM, k0);
+            tma_load_2d(a + 8192, tmA, &full[stage], mt * TC_BM + 64, k0);
           }
           if (B_KMAJOR) {
             if (CL > 1) {  // this CTA's half of the B tile, multicast to the pair
               const int row = p.paired ? (crank == 0 ? nt * (BN / 2) : nt * (BN / 2) + (int)p.pair_off)
                                        : nt * BN + crank * (BN / 2);
-              tma_load_2d_mc(b + crank * (BN / 2) * 128, &tmB, &full[stage], k0, row, kMask);
+              tma_load_2d_mc(b + crank * (BN / 2) * 128, tmB, &full[stage], k0, row, kMask);
             } else if (!p.paired) {
-              tma_load_2d(b, &tmB, &full[stage], k0, nt * BN + (int)(mt * p.b_diag_off));
+              tma_load_2d(b, tmB, &full[stage], k0, nt * BN + (int)(mt * p.b_diag_off));
             } else {
-              tma_load_2d(b, &tmB, &full[stage], k0, nt * (BN / 2));
-              tma_load_2d(b + (BN / 2) * 128, &tmB, &full[stage], k0, nt * (BN / 2) + (int)p.pair_off);
+              tma_load_2d(b, tmB, &full[stage], k0, nt * (BN / 2));
+              tma_load_2d(b + (BN / 2) * 128, tmB, &full[stage], k0, nt * (BN / 2) + (int)p.pair_off);
             }
           } else {
             constexpr int NCH = BN / 64;
@@ -638,9 +653,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               else
                 col = (c < NCH / 2) ? nt * (BN / 2) + c * 64 : nt * (BN / 2) + (int)p.pair_off + (c - NCH / 2) * 64;
               if (CL > 1)
-                tma_load_2d_mc(b + c * 8192, &tmB, &full[stage], col, k0, kMask);
+                tma_load_2d_mc(b + c * 8192, tmB, &full[stage], col, k0, kMask);
               else
-                tma_load_2d(b + c * 8192, &tmB, &full[stage], col, k0);
+                tma_load_2d(b + c * 8192, tmB, &full[stage], col, k0);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -658,8 +673,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
-        int mt, nt, ks;
-        decode_tile_cl(p, t, crank, CL, mt, nt, ks);
+        int mt, nt, ks, grp;
+        decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -703,8 +718,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int NCHUNK_PLAIN = BN / 32;
     constexpr int NCHUNK_PAIR = BN / 64;
     for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
-      int mt, nt, ks;
-      decode_tile_cl(p, t, crank, CL, mt, nt, ks);
+      int mt, nt, ks, grp;
+      decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
+      const CUtensorMap* tmO0 = &mp.o0[NG > 1 ? grp : 0];
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int r0 = mt * TC_BM + quad * 32;
@@ -722,7 +738,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           stage_wait(lane);  // the previous store has read the box
           if (lane == 0) {
             mbar_expect_tx(&rbar[ew], 32 * 32 * 4);
-            tma_load_2d(stg, &tmR, &rbar[ew], n0, r0);
+            tma_load_2d(stg, &mp.r, &rbar[ew], n0, r0);
           }
         }
         // all TMEM columns of the chunk in flight before one wait::ld
@@ -766,7 +782,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             stage_write16(stg, o, outs.prec[slot], hh, lane);
           }
-          stage_commit(stg, slot == 0 ? &tmO0 : (slot == 1 ? &tmO1 : &tmO2), outs.reduce[slot], n0, r0, lane);
+          stage_commit(stg, slot == 0 ? tmO0 : (slot == 1 ? &mp.o1 : &mp.o2), outs.reduce[slot], n0, r0, lane);
         }
       }
       if (!released) {

@@ -224,12 +224,14 @@ __global__ void cast_blockdiag_kernel(const float* __restrict__ src, void* __res
 // dst (2rp x 2f, compute precision) = the block-diagonal expansion of the
 // stacked [Q_g^T ; Q_u^T] (2rp x f, fp32): row block k/rp keeps column block
 // k/rp, the off-diagonal blocks are zero (the transposed low-rank chain).
-__global__ void cast_blockdiag_t_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int rp, int f) {
+// `groups` consecutive (2rp x f) -> (2rp x 2f) blocks (grouped low-rank chain).
+__global__ void cast_blockdiag_t_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int rp, int f,
+                                        int64_t groups) {
   griddep_wait();
-  const int64_t n = (int64_t)4 * rp * f;
+  const int64_t n = groups * 4 * rp * f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = i / (2 * f), c = i % (2 * f);
-    const bool keep = (k < rp) == (c < f);
+    const int64_t k = i / (2 * f), c = i % (2 * f);  // k: global row (group-major)
+    const bool keep = ((k % (2 * rp)) < rp) == (c < f);
     dst[i] = __float2bfloat16_rn(keep ? src[k * f + (c < f ? c : c - f)] : 0.f);
   }
 }

@@ -81,6 +81,13 @@ class StepEngine:
         self.dx = [torch.empty(b, m, **f32) for _ in range(2)]
         self.dx_c = [torch.empty(b, m, dtype=self.dtype, device=self.device) for _ in range(2)] \
             if precision != "fp32" else [None, None]
+        # bf16: the lean blocks' low-rank FFN Wgrads are deferred and run for
+        # all lean layers at once (grouped launches, mecefo_lowrank_wgrads_batched);
+        # each lean layer keeps its output gradient (bf16) and FFN intermediates.
+        self.defer_wgrads = precision == "bf16"
+        self._dyc = [None] * (L + 1)
+        self._saved = [None] * L
+        self._ws_lr = None
         self.xf = torch.empty(b, m, dtype=self.dtype, device=self.device)
         self.inv_f = torch.empty(b, **f32)
         self.logits = torch.empty(b, cfg.vocab, dtype=self.dtype, device=self.device)
@@ -106,6 +113,26 @@ class StepEngine:
                                    self._gp(p + "norm_ffn"), alpha_ffn)
         return _lib.LayerGrads(self._gp(p + "q"), self._gp(p + "o"), self._gp(p + "norm_mha"), alpha_mha,
                                self._gp(p + "gate"), self._gp(p + "down"), self._gp(p + "norm_ffn"), alpha_ffn)
+
+    def _dy_buffer(self, k: int) -> torch.Tensor:
+        """Compute-precision gradient of layer k's input (k = L: the head's
+        output), one persistent buffer per layer (the deferred Wgrads read it)."""
+        if self._dyc[k] is None:
+            self._dyc[k] = torch.empty(self.b * self.max_group, self.cfg.hidden, dtype=self.dtype, device=self.device)
+        return self._dyc[k]
+
+    def _saved_buffers(self, l: int):
+        if self._saved[l] is None:
+            b, m, f = self.b * self.max_group, self.cfg.hidden, self.cfg.ffn_intermediate
+            mk = lambda n: torch.empty(b, n, dtype=self.dtype, device=self.device)
+            self._saved[l] = (mk(m), mk(f), mk(2 * f))
+        return self._saved[l]
+
+    def _lowrank_ws(self, b: int, count: int):
+        n = int(_lib.load().mecefo_lowrank_batched_workspace_bytes(self.eng.handle, b, self.rp, count))
+        if self._ws_lr is None or self._ws_lr.numel() < n:
+            self._ws_lr = torch.empty(n, dtype=torch.uint8, device=self.device)
+        return self._ws_lr.data_ptr(), self._ws_lr.numel()
 
     def _full_cache(self, l: int) -> dict:
         if self.full is None:
@@ -195,27 +222,49 @@ class StepEngine:
                   w.get("final_norm").data_ptr(), w.shadow_view("unembedding").data_ptr(), self.tgt.data_ptr(), b, b1,
                   self.xf.data_ptr(), self.inv_f.data_ptr(), self.logits.data_ptr(), loss_ptr, ws, wn, s)
         cur = 0
+        defer = self.defer_wgrads and any(mb.lean)
+        dxc = (lambda k: self._dy_buffer(k)) if defer else None  # gradient of layer k's input (k = L: head)
         _lib.call("mecefo_head_backward", eng.handle, self.xs[cfg.layers].data_ptr(), w.get("final_norm").data_ptr(),
                   self.inv_f.data_ptr(), self.xf.data_ptr(), self.logits.data_ptr(),
-                  w.shadow_view("unembedding").data_ptr(), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
+                  w.shadow_view("unembedding").data_ptr(), self.dx[cur].data_ptr(),
+                  runtime.ptr(dxc(cfg.layers) if defer else self.dx_c[cur]),
                   self._gp("final_norm"), self._gp("unembedding"), mb.alpha_global, b, ws, wn, s)
+        jobs, keeps = [], []
         for l in reversed(range(cfg.layers)):
             nxt = 1 - cur
+            dyc_in = dxc(l + 1) if defer else self.dx_c[cur]
+            dxc_out = dxc(l) if defer else self.dx_c[nxt]
             g = self._layer_grads(l, mb.alpha_mha[l], mb.alpha_ffn)
             if mb.lean[l]:
                 pst, keep, rp = self._projection(mbs, l)
-                self._keep = keep
-                _lib.call("mecefo_backward_block_neighbor", eng.handle, ctypes.byref(self.lws[l]),
-                          ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
-                          self.dx[nxt].data_ptr(), runtime.ptr(self.dx_c[nxt]), ctypes.byref(g), ctypes.byref(pst), b,
-                          ws, wn, s)
+                keeps.append((pst, keep))
+                if defer:
+                    h2, act, dcat = self._saved_buffers(l)
+                    saved = _lib.FfnSaved(h2.data_ptr(), act.data_ptr(), dcat.data_ptr())
+                    _lib.call("mecefo_backward_block_neighbor_main", eng.handle, ctypes.byref(self.lws[l]),
+                              ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(dyc_in),
+                              self.dx[nxt].data_ptr(), runtime.ptr(dxc_out), ctypes.byref(g), ctypes.byref(saved), b,
+                              ws, wn, s)
+                    jobs.append(_lib.LowrankJob(dyc_in.data_ptr(), saved, ctypes.pointer(pst),
+                                                self._gp(f"layers.{l}.gate"), self._gp(f"layers.{l}.down"),
+                                                mb.alpha_ffn))
+                else:
+                    _lib.call("mecefo_backward_block_neighbor", eng.handle, ctypes.byref(self.lws[l]),
+                              ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(dyc_in),
+                              self.dx[nxt].data_ptr(), runtime.ptr(dxc_out), ctypes.byref(g), ctypes.byref(pst), b,
+                              ws, wn, s)
                 for m_ in mbs:
                     self.proj(m_.rank, l).step += 1
             else:
                 _lib.call("mecefo_backward_block_exact", eng.handle, ctypes.byref(self.lws[l]),
-                          ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(self.dx_c[cur]),
-                          self.dx[nxt].data_ptr(), runtime.ptr(self.dx_c[nxt]), ctypes.byref(g), b, ws, wn, s)
+                          ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(dyc_in),
+                          self.dx[nxt].data_ptr(), runtime.ptr(dxc_out), ctypes.byref(g), b, ws, wn, s)
             cur = nxt
+        if jobs:  # the deferred low-rank FFN Wgrads of every lean layer, grouped
+            arr = (_lib.LowrankJob * len(jobs))(*jobs)
+            wsl, wnl = self._lowrank_ws(b, len(jobs))
+            _lib.call("mecefo_lowrank_wgrads_batched", eng.handle, arr, len(jobs), b, wsl, wnl, s)
+        self._keep = keeps
         _lib.call("mecefo_embedding_backward", eng.handle, self.tok.data_ptr(), self.dx[cur].data_ptr(),
                   self._gp("embedding"), mb.alpha_global, b, s)
 

@@ -172,6 +172,55 @@ def test_fused_lean_microbatches_match_reference(cuda, prec, tol):
     assert all(eng.proj(j, l).step == 2 for j in range(2) for l in range(2))
 
 
+@pytest.mark.parametrize("fused", [True, False])
+def test_deferred_grouped_lowrank_wgrads_match_reference(cuda, fused):
+    """bf16 with r = 128 (rank_pad a multiple of the 128-row tile): every lean
+    layer's low-rank FFN Wgrads are deferred and run as grouped launches
+    (mecefo_lowrank_wgrads_batched); the Eq. (1) gradients equal the
+    reference's per-rank passes + aggregation. fused=False keeps one pass per
+    microbatch (distinct bases per rank -> separate jobs)."""
+    tol = 5e-2
+    batches = _batches(2, 2, seed=13)
+    eng = E.StepEngine(C0, precision="bf16", seqs_per_microbatch=2, r=128, tau=10**6)
+    rng = np.random.Generator(np.random.PCG64(17))
+    bases = {}
+    for j in range(2):
+        for l in range(2):
+            pc = eng.proj(j, l)
+            src = (0, l) if fused else (j, l)
+            if src not in bases:
+                bases[src] = {k: np.linalg.qr(rng.normal(size=(n, 128)))[0]
+                              for k, n in (("gate", 128), ("up", 128), ("down", 344))}
+            for k, v in bases[src].items():
+                pc.set_basis(k, v)
+            pc.step = 1
+            if fused and j == 1:
+                pc.token = eng.proj(0, l).token
+    mbs, lean, skip = _plan(2, {1}, batches)
+    assert eng._fusable(mbs) == fused
+    losses = torch.zeros(2, device="cuda")
+    eng._body(mbs, losses)
+    torch.cuda.synchronize()
+    W = R.init_params(D0, 0)
+    per_rank, ref_losses = [], []
+    for j in range(2):
+        src = (lambda l: (0, l)) if fused else (lambda l: (j, l))
+        loss, g = R.rank_pass(D0, W, batches[j][0], batches[j][1], ["ffn_input_only"] * 2,
+                              {l: bases[src(l)] for l in range(2)})
+        per_rank.append(g)
+        ref_losses.append(loss)
+    active = {(l, k): ([] if k in cluster_ref.MHA else [0, 1]) for l in range(2)
+              for k in cluster_ref.MHA + cluster_ref.FFN}
+    avg, skipped = cluster_ref.aggregate(per_rank, active, 2)
+    assert np.allclose(losses.cpu().numpy(), ref_losses, rtol=tol, atol=tol)
+    for name, shape, off in eng.weights.layout:
+        got = eng.grad[off: off + int(np.prod(shape))].view(shape).cpu().numpy()
+        if name in skipped:
+            assert not got.any(), name
+        else:
+            assert R.rel_err(got, avg[name]) < tol, name
+
+
 def test_batched_refresh_finds_dominant_subspace(cuda):
     """linalg.top_r_right_singular_vectors_batched: the subspace it returns
     for matrices with a spectral gap at r matches numpy's SVD (projector
