@@ -1430,8 +1430,10 @@ int mecefo_head_forward_loss_grouped(mecefo_engine* e, const float* x_last, cons
                                      void* xf, float* inv_f, void* logits, float* loss, void* wsp, size_t ws_bytes,
                                      void* stream) {
   // (Measured: folding softmax statistics into the logits GEMM epilogue made
-  // that GEMM epilogue-bound, 1.17 -> 0.57 PFLOP/s; a separate warp-per-row CE
-  // pass over the L2-resident rows is faster overall.)
+  // that GEMM epilogue-bound, 1.17 -> 0.57 PFLOP/s; chunking the rows so each
+  // chunk's logits stay L2-resident for the CE pass lost 4-13% (small-M
+  // GEMMs and an under-occupied CE per chunk). One logits GEMM + one
+  // warp-per-row CE pass is faster overall.)
   TRY(mecefo_head_logits(e, x_last, final_norm, unemb_c, tokens, xf, inv_f, logits, stream));
   return mecefo_cross_entropy_grouped(e, logits, targets, tokens, group_rows, loss, wsp, ws_bytes, stream);
 }
