@@ -593,55 +593,32 @@ int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const vo
   const int64_t m = e->d.hidden, f = e->d.ffn;
   ProfScope prof("nbr.fused_recompute_swiglu_bwd", 2.0 * b * f * m * 3.0,
                  2.0 * (2.0 * b * m + 3.0 * f * m) + 2.0 * b * f * (act ? 3 : 2), s);
-  CUtensorMap tdy, th2, twd, twgu, tact, tdg, tdu;
+  CUtensorMap tdy, th2, twd, tact, tdg, tdu;
   TRY(make_tmap(e, &tdy, dy_c, m, b, m, 64, TC_BM));
   TRY(make_tmap(e, &th2, h2, m, b, m, 64, TC_BM));
   TRY(make_tmap(e, &twd, w_down_c, f, m, f, 64, 64));
-  TRY(make_tmap(e, &twgu, w_gu_c, m, 2 * f, m, 64, 64));
   std::memset(&tact, 0, sizeof(tact));
   if (act) TRY(make_tmap(e, &tact, act, f, b, f, 32, 32, 0, 64));
   TRY(make_tmap(e, &tdg, dcat, f, b, 2 * f, 32, 32, 0, 64));
   TRY(make_tmap(e, &tdu, reinterpret_cast<uint8_t*>(dcat) + f * 2, f, b, 2 * f, 32, 32, 0, 64));
+  // 128-pair-column kernel (TMEM ring; gemm_dual.cuh)
+  CUtensorMap twgu128;
+  TRY(make_tmap(e, &twgu128, w_gu_c, m, 2 * f, m, 64, 128));
   DualDev p{};
   p.M = (int)b; p.NP = (int)f; p.K = (int)m; p.f_off = f;
   p.kblocks = (int)((m + TC_BK - 1) / TC_BK);
   p.tiles_m = (int)((b + TC_BM - 1) / TC_BM);
-  p.tiles_n = (int)((f + DU_NP - 1) / DU_NP);
+  p.tiles_n = (int)((f + D2_NP - 1) / D2_NP);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.has_act = act ? 1 : 0;
-  // pairs of column tiles share the token operands (multicast); an odd last
-  // column tile computes a zero-padded (TMA OOB) neighbour whose stores are skipped
-  static const bool no_cluster = getenv("MECEFO_NO_CLUSTER") != nullptr;
-  const int CL = (!no_cluster && p.num_tiles >= 2 * kNumSMs) ? 2 : 1;
-  p.tiles_n_cl = (p.tiles_n + CL - 1) / CL;
-  p.num_tiles_cl = p.tiles_m * p.tiles_n_cl;
-  static bool set = false;
-  if (!set) {
-    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
-    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DU_SMEM));
-    set = true;
+  static bool set128 = false;
+  if (!set128) {
+    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D2_SMEM));
+    set128 = true;
   }
-  if (CL == 1) {
-    CUDA_TRY(pdl_launch(swiglu_bwd_dual_kernel<1>, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), DU_SMEM, s,
-                        tdy, th2, twd, twgu, tact, tdg, tdu, p));
-    return check_launch("swiglu_bwd_dual_kernel");
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(CL * std::min(p.num_tiles_cl, kNumSMs / CL)));
-  cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = DU_SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, swiglu_bwd_dual_kernel<2>, tdy, th2, twd, twgu, tact, tdg, tdu, p));
-  return check_launch("swiglu_bwd_dual_kernel<cluster>");
+  CUDA_TRY(pdl_launch(swiglu_bwd_dual128_kernel, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), D2_SMEM, s,
+                      tdy, th2, twd, twgu128, tact, tdg, tdu, p));
+  return check_launch("swiglu_bwd_dual128_kernel");
 }
 
 int cast_to_compute(mecefo_engine* e, const float* src, void* dst, int64_t n, cudaStream_t s) {

@@ -64,8 +64,8 @@ def test_exact_backward_hd64(cuda, prec, tol, T, seqs):
 
 @pytest.mark.parametrize("seqs", [2, 16])
 def test_lean_backward_hd64_lowrank_r128(cuda, seqs):
-    """seqs=16 (4096 tokens) runs the fused recompute kernel in its 2-CTA
-    cluster form (token operands multicast across column-tile pairs)."""
+    """seqs=16 (4096 tokens): many tiles per CTA, so the fused recompute
+    kernel's TMEM ring wraps (d_act of tile i+1 overlapping tile i's epilogue)."""
     cfg, d, W, x, dy = _setup(seqs=seqs)
     rng = np.random.Generator(np.random.PCG64(9))
     basis = {k: np.linalg.qr(rng.normal(size=(n, 128)))[0] for k, n in (("gate", 512), ("up", 512), ("down", 1376))}
