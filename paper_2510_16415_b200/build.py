@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libmecefo.so")
 SOURCES = ["engine.cu"]
-DEPS = ["common.cuh", "gemm.cuh", "kernels.cuh", "attention.cuh", "attention_tc.cuh", "attention_bwd_tc.cuh", "gemm_dual.cuh", "subspace.cuh", "engine.cu"]
+DEPS = ["common.cuh", "gemm.cuh", "kernels.cuh", "attention.cuh", "attention_tc.cuh", "attention_bwd_tc.cuh", "gemm_dual.cuh", "subspace.cuh", "ce.cuh", "engine.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -1,0 +1,142 @@
+// Fused softmax cross-entropy forward + backward over bf16 logits
+// (model.py:492-509) with the row staged in shared memory: each row is read
+// from HBM once (bulk async copy) and dlogits = (softmax - onehot)/n is
+// written once, in place — two HBM passes instead of the three of a
+// register-only kernel whose second read misses L2. NB = 1 row buffer per CTA
+// with several CTAs per SM (one CTA's reductions overlap another's copy;
+// measured faster than NB = 2 double-buffering in one 512-thread CTA).
+#pragma once
+#include <cuda_fp16.h>
+#include "gemm.cuh"
+
+namespace mecefo {
+
+// Two exp2 per MUFU issue (ex2.approx.f16x2): the CE pass is bounded by the
+// SFU (two exps per logit), not HBM. Arguments are <= 0 (x - rowmax), the
+// results in (0, 1] carry 10 mantissa bits — finer than the bf16 dlogits.
+__device__ __forceinline__ float2 ex2_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  uint32_t r;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<uint32_t*>(&h)));
+  return __half22float2(*reinterpret_cast<__half2*>(&r));
+}
+constexpr int CES_COPY_CHUNK = 16384;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void ces_fetch_row(uint8_t* buf, const __nv_bfloat16* row, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of buf precede the copy
+  mbar_expect_tx(bar, bytes);
+  for (uint32_t o = 0; o < bytes; o += CES_COPY_CHUNK)
+    bulk_g2s(buf + o, reinterpret_cast<const uint8_t*>(row) + o, min((uint32_t)CES_COPY_CHUNK, bytes - o), bar);
+}
+
+// dynamic smem: 2 row buffers (V*2 bytes, 128-B aligned) + 2 mbarriers + reduction scratch
+template <int NB, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    cross_entropy_smem_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld, const int64_t* __restrict__ targets,
+                              float* __restrict__ loss_rows, int rows, int V, float inv_n, int* __restrict__ bad_target) {
+  extern __shared__ __align__(128) uint8_t ces_smem[];
+  const uint32_t rb = (uint32_t)V * 2;
+  const uint32_t rb_al = (rb + 127) & ~127u;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ces_smem + NB * rb_al);
+  float* red = reinterpret_cast<float*>(bars + 2);  // [2][NT/32]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  griddep_wait();
+  const int nvec = V >> 3;
+  if (tid == 0 && (int)blockIdx.x < rows) ces_fetch_row(ces_smem, logits + (int64_t)blockIdx.x * ld, rb, &bars[0]);
+  int it = 0;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+    const int cur = NB == 2 ? (it & 1) : 0;
+    const int rn = r + gridDim.x;
+    if (NB == 2 && tid == 0 && rn < rows)
+      ces_fetch_row(ces_smem + (cur ^ 1) * rb_al, logits + (int64_t)rn * ld, rb, &bars[cur ^ 1]);
+    mbar_wait(&bars[cur], NB == 2 ? ((it >> 1) & 1) : (it & 1));
+    const int64_t t = targets[r];
+    const bool tgt_ok = t >= 0 && t < V;
+    if (!tgt_ok && tid == 0) atomicExch(bad_target, 1);
+    const uint8_t* bufc = ces_smem + cur * rb_al;
+    const uint4* sv = reinterpret_cast<const uint4*>(bufc);
+    // pass 1 (smem): per-thread online (max, sum exp)
+    float mx = -INFINITY, s = 0.f;
+    for (int vi = tid; vi < nvec; vi += NT) {
+      const uint4 w = sv[vi];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+      float f[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 q = __bfloat1622float2(h[j]);
+        f[2 * j] = q.x;
+        f[2 * j + 1] = q.y;
+      }
+      float lm = f[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) lm = fmaxf(lm, f[j]);
+      const float nm = fmaxf(mx, lm);
+      s = (mx == -INFINITY) ? 0.f : s * __expf(mx - nm);
+      const float nml = nm * 1.4426950408889634f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 e2 = ex2_h2(fmaf(f[2 * j], 1.4426950408889634f, -nml), fmaf(f[2 * j + 1], 1.4426950408889634f, -nml));
+        s += e2.x + e2.y;
+      }
+      mx = nm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+      const float os = __shfl_xor_sync(0xffffffffu, s, o);
+      const float nm = fmaxf(mx, om);
+      s = (mx == -INFINITY ? 0.f : s * __expf(mx - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+      mx = nm;
+    }
+    if (lane == 0) {
+      red[warp] = mx;
+      red[NW + warp] = s;
+    }
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red[w]);
+    s = 0.f;
+    for (int w = 0; w < NW; ++w) s += red[NW + w] * __expf(red[w] - mx);
+    const __nv_bfloat16* srow = reinterpret_cast<const __nv_bfloat16*>(bufc);
+    if (tid == 0) loss_rows[r] = tgt_ok ? mx + logf(s) - __bfloat162float(srow[t]) : 0.f;
+    // pass 2: dlogits from smem, one HBM write
+    const float sc = inv_n / s;
+    const float mxl = mx * 1.4426950408889634f;
+    uint4* gw = reinterpret_cast<uint4*>(logits + (int64_t)r * ld);
+    for (int vi = tid; vi < nvec; vi += NT) {
+      const uint4 w = sv[vi];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+      uint32_t o4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 q = __bfloat1622float2(h[j]);
+        const float2 e2 = ex2_h2(fmaf(q.x, 1.4426950408889634f, -mxl), fmaf(q.y, 1.4426950408889634f, -mxl));
+        float p0 = e2.x * sc, p1 = e2.y * sc;
+        const int c = vi * 8 + 2 * j;
+        if (c == t) p0 -= inv_n;
+        if (c + 1 == t) p1 -= inv_n;
+        __nv_bfloat162 rr = __floats2bfloat162_rn(p0, p1);
+        o4[j] = *reinterpret_cast<uint32_t*>(&rr);
+      }
+      gw[vi] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    }
+    __syncthreads();  // this buffer and red are free for the next-but-one row
+    if (NB == 1 && tid == 0 && rn < rows) ces_fetch_row(ces_smem, logits + (int64_t)rn * ld, rb, &bars[0]);
+  }
+}
+
+}  // namespace mecefo
