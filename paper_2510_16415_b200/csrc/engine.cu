@@ -769,7 +769,10 @@ int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims) {
   e->ps = d.precision == MECEFO_PREC_BF16 ? 2 : 4;
   const int hd = (int)(d.hidden / d.heads);
   const int half = std::max(1, hd / 2);
-  std::vector<float> c((size_t)d.seq_len * half), sn((size_t)d.seq_len * half);
+  // cos table followed by the `half` frequencies theta_j (fp32) that the tcgen05
+  // QKV epilogue uses to compute its angles
+  std::vector<float> c((size_t)d.seq_len * half + half), sn((size_t)d.seq_len * half);
+  for (int j = 0; j < half; ++j) c[(size_t)d.seq_len * half + j] = (float)std::pow(10000.0, -2.0 * j / hd);
   for (int64_t t = 0; t < d.seq_len; ++t)
     for (int j = 0; j < half; ++j) {
       const double theta = std::pow(10000.0, -2.0 * j / hd);  // model.py:274
@@ -839,6 +842,7 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   if (e->d.rope) {  // q, k leave the GEMM rotated (model.py:323-326)
     g.epi.rope_cos = e->rope_cos; g.epi.rope_sin = e->rope_sin;
     g.epi.rope_T = (int)e->d.seq_len; g.epi.rope_hd = (int)(m / e->d.heads); g.epi.rope_cols = (int)(2 * m);
+    g.epi.rope_theta = e->rope_cos + e->d.seq_len * (g.epi.rope_hd / 2);
   }
   g.tag = "fwd.qkv";
   TRY(run_gemm(e, g, s));

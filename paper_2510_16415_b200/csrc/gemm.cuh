@@ -49,6 +49,7 @@ struct Epilogue {
   // interleaved (even, odd) pairs rotated by pos * theta_j, pos = row % rope_T.
   const float* rope_cos;
   const float* rope_sin;
+  const float* rope_theta;  // theta_j, j < hd/2 (tcgen05 epilogue computes the angles)
   int rope_T, rope_hd, rope_cols;
 };
 
@@ -488,11 +489,13 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
         // (model.py:274); |angle error| <= ~6e-5 rad after Cody-Waite
         // reduction to [-pi, pi], far below the bf16 rounding of q/k.
         const int j0 = (n0 % e.rope_hd) >> 1;
-        const float ls = -26.575424759098898f / (float)e.rope_hd;  // -2 log2(10000) / hd
         const float fpos = (float)pos;
+        float th[8];  // 128-B table: stays L1-resident (the cos/sin table did not)
+        *reinterpret_cast<float4*>(th) = __ldg(reinterpret_cast<const float4*>(e.rope_theta + j0));
+        *reinterpret_cast<float4*>(th + 4) = __ldg(reinterpret_cast<const float4*>(e.rope_theta + j0 + 4));
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float ang = fpos * exp2f((float)(j0 + j) * ls);
+          const float ang = fpos * th[j];
           const float kq = rintf(ang * 0.15915494309189535f);
           float rr = fmaf(-kq, 6.28318548202514648f, ang);
           rr = fmaf(kq, 1.7484556e-7f, rr);
