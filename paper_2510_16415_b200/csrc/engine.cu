@@ -264,7 +264,7 @@ Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, floa
   return e;
 }
 
-template <int BN, bool AK, bool BKM, int CL, int NG>
+template <int BN, bool AK, bool BKM, int CL, int NG, bool ROPE = false>
 int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   using C = TcCfg<BN>;
   static_assert(NG == 1 || CL == 1, "grouped launches are single-CTA");
@@ -349,7 +349,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     static const bool no_res = getenv("MECEFO_DBG_NORES") != nullptr;
     if (no_res) p.epi.residual = nullptr;
   }
-  auto kern = gemm_tc_kernel<BN, AK, BKM, CL, NG>;
+  auto kern = gemm_tc_kernel<BN, AK, BKM, CL, NG, ROPE>;
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -453,6 +453,8 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   if (e->prec == PREC_BF16) {
     if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
     const int BN = choose_bn(g);
+    if (g.epi.rope_cos && BN == 256 && g.a.km && g.b.km && !g.paired && !use_cluster(g, BN))
+      return launch_tc<256, true, true, 1, 1, true>(e, g, s);  // QKV with RoPE (per-tile angle table)
     const bool cl = use_cluster(g, BN);
     if (BN == 256) return cl ? dispatch_tc_major<256, 2>(e, g, s) : dispatch_tc_major<256, 1>(e, g, s);
     if (BN == 128) return cl ? dispatch_tc_major<128, 2>(e, g, s) : dispatch_tc_major<128, 1>(e, g, s);

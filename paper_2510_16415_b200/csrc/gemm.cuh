@@ -475,7 +475,8 @@ __device__ __forceinline__ void stage_store32_db(uint8_t* stg, int& sb, const CU
 // Epilogue math for output slot `slot` on 16 consecutive output columns n0..
 // of row r (tcgen05 path): 0 = out / act, 1 = gate or d_gate, 2 = up or d_up.
 __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, int n0, int cnt, bool row_ok,
-                                           const float* g, const float* u, float* o, bool res_in_smem = false) {
+                                           const float* g, const float* u, float* o, bool res_in_smem = false,
+                                           const float* rope_pre = nullptr) {
   if (e.kind == EPI_STORE || e.kind == EPI_ATOMIC) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) o[j] = g[j] * e.alpha;
@@ -488,6 +489,16 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
         // latency was serialising the epilogue. theta_j = 10000^(-2j/hd)
         // (model.py:274); |angle error| <= ~6e-5 rad after Cody-Waite
         // reduction to [-pi, pi], far below the bf16 rounding of q/k.
+        if (rope_pre) {  // this row's (cos, sin) of these 8 frequencies, computed once per tile
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float cs = rope_pre[j], sn = rope_pre[16 + j];
+            const float ev = o[2 * j], od = o[2 * j + 1];
+            o[2 * j] = ev * cs - od * sn;
+            o[2 * j + 1] = ev * sn + od * cs;
+          }
+          return;
+        }
         const int j0 = (n0 % e.rope_hd) >> 1;
         const float fpos = (float)pos;
         float th[8];  // 128-B table: stays L1-resident (the cos/sin table did not)
@@ -561,7 +572,7 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
     o[j] = slot == 2 ? d[j] * silu_f(g[j]) : (d[j] * u[j]) * silu_grad_f(g[j]);
 }
 
-template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL, int NG>
+template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL, int NG, bool ROPE = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ TcMaps<NG> mp, GemmDev p, TcOut outs) {
   using C = TcCfg<BN>;
@@ -733,6 +744,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
       const int cbase = p.paired ? nt * (BN / 2) : nt * BN;
       bool released = false;
+      // hd = 64 RoPE: every chunk this warp handles (c = half + 2k, 32 columns)
+      // uses the same 16 frequencies j = 16*half + i, so the row's (cos, sin)
+      // are computed once per tile instead of once per head
+      // (ROPE instantiation only: the 32 extra registers would spill elsewhere)
+      float rcs[ROPE ? 32 : 1];
+      const bool rope_pre = ROPE && p.epi.rope_cos && p.epi.rope_hd == 64 && (BN % 64) == 0 && !p.paired &&
+                            cbase < p.epi.rope_cols && row_ok;
+      if constexpr (ROPE) if (rope_pre) {
+        const float fpos = (float)(row % p.epi.rope_T);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float ang = fpos * __ldg(p.epi.rope_theta + half * 16 + i);
+          const float kq = rintf(ang * 0.15915494309189535f);
+          float rr = fmaf(-kq, 6.28318548202514648f, ang);
+          rr = fmaf(kq, 1.7484556e-7f, rr);
+          __sincosf(rr, &rcs[16 + i], &rcs[i]);
+        }
+      }
 #pragma unroll 1
       for (int c = half; c < nchunks; c += 2) {
         const int n0 = cbase + c * 32;
@@ -774,7 +803,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int hh = 0; hh < 2; ++hh) {
             float o[16];
             const int n0h = n0 + hh * 16;
-            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g + hh * 16, u + hh * 16, o, rs);
+            const float* rp = nullptr;
+            if constexpr (ROPE) rp = (rope_pre && n0h + 16 <= p.epi.rope_cols) ? rcs + hh * 8 : nullptr;
+            epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g + hh * 16, u + hh * 16, o, rs, rp);
             if (rs) {  // + residual from the staging box (this lane's row, 16 columns)
               const uint8_t* rrow = stg + lane * 128;
 #pragma unroll
