@@ -724,6 +724,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // fp32 residual (x + f(x) epilogues): the 32x32 residual box is TMA-loaded
     // into the staging box (same SW128 layout as the fp32 store), added in
     // place, and stored — no per-lane strided global reads in the epilogue
+    // (measured: prefetching each lane's row segment into registers one chunk
+    // ahead was 13% slower than this)
     const bool res_tma = p.epi.kind == EPI_STORE && p.epi.residual != nullptr && outs.used[0] &&
                          outs.prec[0] == PREC_F32 && !p.paired;
     uint32_t rphase = 0;
