@@ -243,9 +243,11 @@ struct GemmCall {
   int split = 1;
   const char* tag = "gemm";
   int force_bn = 0;  // tcgen05 tile width override (split-K accumulate GEMMs)
-  // block-diagonal batching: M tile mt reads B columns shifted by mt * b_diag_off
-  // (two independent products sharing one launch; needs 128-row blocks)
+  // block-diagonal batching: M tile mt reads B columns shifted by
+  // (mt / b_diag_div) * b_diag_off (independent products sharing one launch;
+  // each diagonal block spans b_diag_div whole 128-row tiles)
   int64_t b_diag_off = 0;
+  int b_diag_div = 1;
   // grouped launch: `groups` products of this shape, operand/output base
   // pointers per group (ga/gb/go override a.p/b.p/epi.out); same strides
   int groups = 1;
@@ -272,7 +274,8 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   if (ng < 1 || ng > NG) return set_err(MECEFO_ERR_CONSISTENCY, "group count %d outside [1, %d]", ng, NG);
   TcMaps<NG> mp;
   std::memset(&mp, 0, sizeof(mp));
-  const int64_t rowsB = g.paired ? g.pair_off + g.N : g.N + g.b_diag_off * ((g.M + TC_BM - 1) / TC_BM - 1);
+  const int64_t rowsB =
+      g.paired ? g.pair_off + g.N : g.N + g.b_diag_off * (((g.M + TC_BM - 1) / TC_BM - 1) / std::max(1, g.b_diag_div));
   for (int q = 0; q < ng; ++q) {
     const void* pa = NG > 1 ? g.ga[q] : g.a.p;
     const void* pb = NG > 1 ? g.gb[q] : g.b.p;
@@ -286,6 +289,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   p.paired = g.paired ? 1 : 0;
   p.pair_off = g.pair_off;
   p.b_diag_off = g.b_diag_off;
+  p.b_diag_div = std::max(1, g.b_diag_div);
   p.kblocks = (int)((g.K + TC_BK - 1) / TC_BK);
   int split = std::max(1, std::min(g.split, p.kblocks));
   p.kb_per_split = (p.kblocks + split - 1) / split;
@@ -927,6 +931,7 @@ int lowrank_ffn_wgrads(mecefo_engine* e, Ws& ws, const mecefo_projection* pj, co
     g.M = 2 * rp; g.N = f; g.K = b;
     g.a = {P, 2 * rp, false}; g.b = {dcat, 2 * f, false};
     g.b_diag_off = f;
+    g.b_diag_div = (int)(rp / TC_BM);  // rows [0, rp) meet d_gate, [rp, 2rp) d_up
     g.tag = "lowrank.Q_gu";
     TRY(gemm_accumulate(e, g, QT, f, 1.f, s));
     {
@@ -1666,6 +1671,7 @@ int mecefo_lowrank_wgrads_batched(mecefo_engine* e, const mecefo_lowrank_job* jo
     g.M = 2 * rp; g.N = f; g.K = b;
     g.a = {Pq(0), 2 * rp, false}; g.b = {J[0].saved.dcat, 2 * f, false};
     g.b_diag_off = f;
+    g.b_diag_div = (int)(rp / TC_BM);  // rows [0, rp) meet d_gate, [rp, 2rp) d_up
     g.groups = n;
     for (int q = 0; q < n; ++q) { g.ga[q] = Pq(q); g.gb[q] = J[q].saved.dcat; g.go[q] = QT + (size_t)q * 2 * rp * f; }
     g.tag = "lowrank.Q";

@@ -57,7 +57,8 @@ struct GemmDev {
   int M, N, K;           // N = logical output columns (pair columns in paired mode)
   int paired;            // 0/1
   int64_t pair_off;      // B row offset of the second accumulator (paired)
-  int64_t b_diag_off;    // block-diagonal batching: M tile mt reads B N-coordinates + mt * b_diag_off
+  int64_t b_diag_off;    // block-diagonal batching: M tile mt reads B N-coordinates + (mt / b_diag_div) * b_diag_off
+  int b_diag_div;        // M tiles per diagonal block (>= 1)
   int split;             // number of K splits
   int kb_per_split;      // k-blocks (of 64) per split
   int kblocks;           // total k-blocks
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                        : nt * BN + crank * (BN / 2);
               tma_load_2d_mc(b + crank * (BN / 2) * 128, tmB, &full[stage], k0, row, kMask);
             } else if (!p.paired) {
-              tma_load_2d(b, tmB, &full[stage], k0, nt * BN + (int)(mt * p.b_diag_off));
+              tma_load_2d(b, tmB, &full[stage], k0, nt * BN + (int)((mt / p.b_diag_div) * p.b_diag_off));
             } else {
               tma_load_2d(b, tmB, &full[stage], k0, nt * (BN / 2));
               tma_load_2d(b + (BN / 2) * 128, tmB, &full[stage], k0, nt * (BN / 2) + (int)p.pair_off);
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (CL > 1 && c / (NCH / CL) != crank) continue;
               int col;
               if (!p.paired)
-                col = nt * BN + c * 64 + (int)(mt * p.b_diag_off);
+                col = nt * BN + c * 64 + (int)((mt / p.b_diag_div) * p.b_diag_off);
               else
                 col = (c < NCH / 2) ? nt * (BN / 2) + c * 64 : nt * (BN / 2) + (int)p.pair_off + (c - NCH / 2) * 64;
               if (CL > 1)

@@ -84,3 +84,31 @@ def test_lean_backward_hd64_lowrank_r128(cuda, seqs):
     assert R.rel_err(dx.cpu().numpy(), dx_ref.reshape(x.shape)) < BF16_TOL
     for k in g:
         assert R.rel_err(g[k].cpu().numpy(), g_ref[k]) < BF16_TOL, k
+
+
+@pytest.mark.parametrize("hidden,heads,ffn,r", [(768, 12, 2048, 128), (1024, 16, 2736, 128),
+                                                (2048, 32, 5472, 64), (2048, 32, 5472, 256)])
+def test_lean_backward_llama_shapes(cuda, hidden, heads, ffn, r):
+    """SURVEY configs C2 (130M), C3 (350M) and C4 (1B, r in {64, 256}) block
+    shapes: one lean block forward + neighbour backward in bf16 vs the fp64
+    oracle. ffn 2736 / 5472 leave partial 128-column tiles; r = 256 makes the
+    transposed low-rank contraction's diagonal blocks two tiles tall."""
+    cfg, d, W, x, dy = _setup(hidden=hidden, heads=heads, ffn=ffn, T=256, seqs=1)
+    rng = np.random.Generator(np.random.PCG64(21))
+    basis = {k: np.linalg.qr(rng.normal(size=(n, r)))[0] for k, n in (("gate", hidden), ("up", hidden),
+                                                                         ("down", ffn))}
+    _, lean_ref = R.block_fwd(d, W, 0, x.reshape(1, 256, -1), lean=True)
+    dx_ref, g_ref = R.block_bwd_neighbor(d, W, 0, lean_ref, dy.reshape(1, 256, -1), basis)
+    w = mdl.init_weights(cfg, 0, precision="bf16")
+    _, cache = mdl.forward_block(cfg, w.layers[0], torch.tensor(x, dtype=torch.float32, device="cuda"),
+                                 mdl.CACHE_FFN_INPUT_ONLY)
+    proj = approx.ProjectionCache(rank=r, refresh_period=10**9, step=1)
+    for k, v in basis.items():
+        proj.set_basis(k, v)
+    from paper_2510_16415_b200.linalg import SvdConfig
+    dx, g = approx.backward_block_neighbor(cfg, w.layers[0], cache,
+                                           torch.tensor(dy, dtype=torch.float32, device="cuda"), proj=proj,
+                                           svd=SvdConfig(rank=r))
+    assert R.rel_err(dx.cpu().numpy(), dx_ref.reshape(x.shape)) < BF16_TOL
+    for k in g:
+        assert R.rel_err(g[k].cpu().numpy(), g_ref[k]) < BF16_TOL, k
