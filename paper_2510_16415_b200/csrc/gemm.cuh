@@ -632,6 +632,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
         const CUtensorMap* tmA = &mp.a[NG > 1 ? grp : 0];
         const CUtensorMap* tmB = &mp.b[NG > 1 ? grp : 0];
+        // once per tile: this single thread issues every TMA of the k-loop, so
+        // nothing per k-block may cost more than a few instructions
+        const int boff = p.b_diag_off ? (int)((mt / p.b_diag_div) * p.b_diag_off) : 0;
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                        : nt * BN + crank * (BN / 2);
               tma_load_2d_mc(b + crank * (BN / 2) * 128, tmB, &full[stage], k0, row, kMask);
             } else if (!p.paired) {
-              tma_load_2d(b, tmB, &full[stage], k0, nt * BN + (int)((mt / p.b_diag_div) * p.b_diag_off));
+              tma_load_2d(b, tmB, &full[stage], k0, nt * BN + boff);
             } else {
               tma_load_2d(b, tmB, &full[stage], k0, nt * (BN / 2));
               tma_load_2d(b + (BN / 2) * 128, tmB, &full[stage], k0, nt * (BN / 2) + (int)p.pair_off);
@@ -664,7 +667,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (CL > 1 && c / (NCH / CL) != crank) continue;
               int col;
               if (!p.paired)
-                col = nt * BN + c * 64 + (int)((mt / p.b_diag_div) * p.b_diag_off);
+                col = nt * BN + c * 64 + boff;
               else
                 col = (c < NCH / 2) ? nt * (BN / 2) + c * 64 : nt * (BN / 2) + (int)p.pair_off + (c - NCH / 2) * 64;
               if (CL > 1)
