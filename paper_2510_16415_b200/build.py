@@ -1,4 +1,5 @@
-"""Build libmecefo.so in-tree with nvcc for sm_100a (no JIT cache, no torch ext).
+"""Build libmecefo.so in-tree with nvcc for sm_100a (no JIT cache, no torch ext),
+and the host-only control-plane library libmecefo_ctl.so with g++.
 
 Usage: python -m paper_2510_16415_b200.build [--force]
 """
@@ -38,7 +39,26 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in files)
 
 
+CTL_OUT = os.path.join(HERE, "libmecefo_ctl.so")
+CTL_SOURCES = [os.path.join(CSRC, "control.cpp"), os.path.join(ROOT, "include", "mecefo_ctl.h")]
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-I", os.path.join(ROOT, "include")]
+
+
+def build_control(force: bool = False, verbose: bool = True) -> str:
+    """g++ include/mecefo_ctl.h + csrc/control.cpp -> libmecefo_ctl.so (host PCG64 streams)."""
+    if not force and os.path.exists(CTL_OUT) and all(os.path.getmtime(f) <= os.path.getmtime(CTL_OUT)
+                                                     for f in CTL_SOURCES):
+        return CTL_OUT
+    cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-o", CTL_OUT + ".tmp", CTL_SOURCES[0]]
+    if verbose:
+        print("[build]", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(CTL_OUT + ".tmp", CTL_OUT)
+    return CTL_OUT
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
+    build_control(force, verbose)
     if not force and not stale():
         return OUT
     cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]

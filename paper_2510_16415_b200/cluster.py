@@ -22,6 +22,7 @@ from typing import Iterable
 import numpy as np
 
 from .errors import ConfigError, ConsistencyError, ContractViolation, UnrecoverableRankError
+from .pcg import Pcg64Generator
 
 HEALTHY = "healthy"
 FAILED = "failed"
@@ -143,7 +144,8 @@ class ClusterState:
     def __init__(self, cfg: ClusterConfig, scenario: FailureScenario):
         self.cfg = cfg
         self.scenario = scenario
-        self.rng = np.random.Generator(np.random.PCG64(scenario.seed))
+        # native PCG64 (libmecefo_ctl.so), draw-for-draw == Generator(PCG64(seed)) of cluster.py:98
+        self.rng = Pcg64Generator(scenario.seed)
         self._st = np.zeros((cfg.dp, cfg.pp), dtype=np.int8)
         self._ex = np.tile(np.arange(cfg.pp, dtype=np.int32), (cfg.dp, 1))
         self.down_until: dict = {}

@@ -27,6 +27,7 @@ import torch
 from . import approx, cluster as cl, costmodel as cm, engine as E, model as mdl, optim as op
 from .errors import ConfigError, NumericalFailure
 from .linalg import SvdConfig
+from .pcg import Pcg64Generator
 
 METRICS_HEADER = "iteration,loss,perplexity,rho1,rho2,lr,sim_time_s,affected_ranks"
 
@@ -211,8 +212,7 @@ class SyntheticSampler:
 
     def __init__(self, n_ranks: int, seq_len: int, vocab: int, seed: int):
         self.T, self.V = seq_len, vocab
-        self.rngs = [np.random.Generator(np.random.PCG64(np.random.SeedSequence((seed, 0x5E7, i))))
-                     for i in range(n_ranks)]
+        self.rngs = [Pcg64Generator((seed, 0x5E7, i)) for i in range(n_ranks)]  # native PCG64 streams
 
     def batch(self, rank: int, n: int):
         x = self.rngs[rank].integers(0, self.V, size=(n, self.T + 1))
