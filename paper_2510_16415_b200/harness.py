@@ -207,8 +207,9 @@ class RunResult:
 
 class SyntheticSampler:
     """LLaMA-shaped synthetic batches: uniform tokens, next-token targets,
-    one PCG64 stream per DP rank (the corpus sampler of data.py is out of
-    scope; any object with .batch(rank, n) -> (tokens, targets) plugs in)."""
+    one native PCG64 stream per DP rank. The reference's corpus/teacher sampler
+    is data.ShardedSampler; any object with .batch(rank, n) -> (tokens, targets)
+    plugs in."""
 
     def __init__(self, n_ranks: int, seq_len: int, vocab: int, seed: int):
         self.T, self.V = seq_len, vocab

@@ -87,3 +87,44 @@ def test_cluster_state_uses_native_stream():
     st = cluster.ClusterState(cluster.ClusterConfig(dp=4, pp=2, layers=2), cluster.FailureScenario(kind="per_iteration",
                                                                                         probability=0.5, seed=7))
     assert isinstance(st.rng, pcg.Pcg64Generator)
+
+
+def _sampler_golden():
+    import json
+
+    return json.load(open(os.path.join(ROOT, "tests", "golden", "sampler.json")))
+
+
+@pytest.mark.parametrize("source", ["teacher", "corpus"])
+def test_sharded_sampler_matches_reference_batches(source):
+    """data.ShardedSampler == reference faultsim.data.ShardedSampler
+    (tests/golden/make_sampler_golden.py): same shards, same window starts
+    from the native (seed, 0xDA7A, rank) streams, bit-exact token ids."""
+    from paper_2510_16415_b200 import data
+
+    rec = _sampler_golden()[source]
+    args = dict(rec["args"])
+    if source == "corpus":
+        args["text"] = rec["text"]
+    s = data.ShardedSampler(**args)
+    for call in rec["calls"]:
+        x, y = s.batch(call["rank"], call["batch"])
+        assert x.dtype == np.int64 and x.shape == (call["batch"], args["seq_len"])
+        assert x.tolist() == call["inputs"] and y.tolist() == call["targets"]
+    ex, ey = s.eval_windows(0, 5)
+    assert ex.tolist() == rec["eval"]["inputs"] and ey.tolist() == rec["eval"]["targets"]
+
+
+def test_sharded_sampler_contract():
+    from paper_2510_16415_b200 import data
+
+    with pytest.raises(errors.ConfigError):
+        data.ShardedSampler(2, 8, 16, 0, source="corpus")  # no corpus given
+    with pytest.raises(errors.ConfigError):
+        data.ShardedSampler(2, 8, 2, 0, source="corpus", text="abcabc" * 20)  # vocab too small
+    with pytest.raises(errors.ConfigError):
+        data.ShardedSampler(2, 40, 16, 0, source="corpus", text="ab" * 30)  # shard too short
+    with pytest.raises(errors.ConfigError):
+        data.ShardedSampler(2, 8, 16, 0, source="bogus")
+    with pytest.raises(errors.ConfigError):
+        data.encode("abz", {"a": 0, "b": 1})
