@@ -291,4 +291,70 @@ def run_training(cfg: RunConfig, out_dir: str | None = None, quiet: bool = True,
     finally:
         metrics.flush()
         events_out.flush()
+    if out_dir:
+        dump_weights(weights, out_dir)  # harness.py:468-469
     return RunResult(rows=rows, events=all_events, weights=weights, summary=_summary(rows))
+
+
+# --- weight wire format (harness.py:635-665: final_weights.bin + .json) -----
+
+def pack_weights(layout, master: np.ndarray):
+    """Canonical-order dense little-endian float64 blob + manifest from the
+    aligned flat parameter store (padding between groups dropped)."""
+    params, chunks, off = [], [], 0
+    for name, shape, src in layout:
+        n = int(np.prod(shape))
+        params.append({"name": name, "shape": list(shape), "offset_elems": off})
+        chunks.append(master[src: src + n])
+        off += n
+    blob = np.concatenate(chunks).astype("<f8") if chunks else np.zeros(0, "<f8")
+    return blob, {"dtype": "<f8", "total_elems": off, "params": params}
+
+
+def unpack_weights(layout, total: int, blob: np.ndarray, manifest: dict) -> np.ndarray:
+    """Inverse of pack_weights into an aligned fp32 flat store; names and
+    shapes must match the model's layout (ContractViolation otherwise)."""
+    from .errors import ContractViolation
+
+    want = {name: (tuple(shape), src) for name, shape, src in layout}
+    host = np.zeros(total, dtype=np.float32)
+    seen = set()
+    for e in manifest["params"]:
+        name, shape = e["name"], tuple(e["shape"])
+        if name not in want or want[name][0] != shape:
+            raise ContractViolation(f"final_weights.json: unexpected parameter {name} {shape}")
+        n = int(np.prod(shape))
+        start = int(e["offset_elems"])
+        if start + n > blob.size:
+            raise ContractViolation(f"final_weights.bin too short for {name}")
+        host[want[name][1]: want[name][1] + n] = blob[start: start + n]
+        seen.add(name)
+    missing = set(want) - seen
+    if missing:
+        raise ContractViolation(f"final_weights.json lacks {sorted(missing)[:3]}")
+    return host
+
+
+def dump_weights(weights: mdl.ModelWeights, out_dir: str) -> None:
+    """harness.py:635-651: one device->host copy of the fp32 master store,
+    written as final_weights.bin (<f8, canonical order) + final_weights.json."""
+    os.makedirs(out_dir, exist_ok=True)
+    blob, manifest = pack_weights(weights.layout, weights.master.detach().cpu().numpy())
+    tmp = os.path.join(out_dir, "final_weights.bin.tmp")
+    blob.tofile(tmp)
+    os.replace(tmp, os.path.join(out_dir, "final_weights.bin"))
+    with open(os.path.join(out_dir, "final_weights.json"), "w", encoding="utf-8") as f:
+        json.dump(manifest, f, indent=2)
+
+
+def load_weights(cfg: mdl.ModelConfig, out_dir: str, precision: str = "fp32") -> mdl.ModelWeights:
+    """harness.py:654-665: read the dump back into a device store (one
+    host->device copy, then the compute-precision shadow is refreshed)."""
+    with open(os.path.join(out_dir, "final_weights.json"), "r", encoding="utf-8") as f:
+        manifest = json.load(f)
+    blob = np.fromfile(os.path.join(out_dir, "final_weights.bin"), dtype="<f8")
+    w = mdl.ModelWeights(cfg, precision)
+    host = unpack_weights(w.layout, w.total, blob, manifest)
+    w.master.copy_(torch.from_numpy(host).to(w.device))
+    w.sync_shadow()
+    return w

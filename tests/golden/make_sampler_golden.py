@@ -2,7 +2,8 @@
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_sampler_golden.py
 
-Writes tests/golden/sampler.json: for the teacher source and for a corpus
+Writes tests/golden/sampler.json and weights_manifest.json (C0 final_weights.json
+of the reference dump_weights). sampler.json: for the teacher source and for a corpus
 source over a synthetic text (written to a temp file, so the reference's
 embedded asset is not needed), three batch() calls per rank plus
 eval_windows(). Nothing at test time imports the reference.
@@ -58,3 +59,27 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def weights_manifest():
+    """final_weights.json of the reference dump for C0 init weights (seed 0),
+    plus sha256 of the dumped blob rounded to float32 (the engine's master
+    precision): tests/golden/weights_manifest.json."""
+    import hashlib
+
+    import numpy as np
+
+    from faultsim import harness, model as mdl
+
+    cfg = mdl.ModelConfig(vocab=64, hidden=128, heads=4, ffn_intermediate=344, layers=2, seq_len=64, rope=True)
+    with tempfile.TemporaryDirectory() as d:
+        harness.dump_weights(mdl.init_weights(cfg, seed=0), d)
+        manifest = json.load(open(os.path.join(d, "final_weights.json")))
+        blob = np.fromfile(os.path.join(d, "final_weights.bin"), dtype="<f8")
+    manifest["sha256_f32"] = hashlib.sha256(blob.astype("<f4").tobytes()).hexdigest()
+    with open(os.path.join(OUT, "weights_manifest.json"), "w") as fh:
+        json.dump(manifest, fh)
+
+
+if __name__ == "__main__":
+    weights_manifest()
