@@ -126,6 +126,37 @@ def config_from_dict(raw: dict) -> RunConfig:
     return cfg
 
 
+def load_config(path: str) -> RunConfig:
+    """harness.py:153-159."""
+    try:
+        with open(path, "r", encoding="utf-8") as f:
+            raw = json.load(f)
+    except (OSError, json.JSONDecodeError) as exc:
+        raise ConfigError(f"cannot read config {path}: {exc}") from exc
+    return config_from_dict(raw)
+
+
+def replace_scenario_seed(cfg: RunConfig, seed: int) -> RunConfig:
+    """harness.py:131-150: same run, failure stream reseeded."""
+    sc = cfg.scenario
+    new_sc = cl.FailureScenario(kind=sc.kind, probability=sc.probability, recovery_iterations=sc.recovery_iterations,
+                                failure_interval_s=sc.failure_interval_s, recovery_time_s=sc.recovery_time_s,
+                                victims=sc.victims, seed=seed)
+    return RunConfig(model=cfg.model, cluster=cfg.cluster, scenario=new_sc, optimizer=cfg.optimizer, run=cfg.run,
+                     cost=cfg.cost, data=cfg.data)
+
+
+def make_sampler(cfg: RunConfig):
+    """harness.py:300-307: data.source "corpus"/"teacher" -> data.ShardedSampler
+    (bit-exact batches); "synthetic" (this engine's default) -> SyntheticSampler."""
+    if cfg.data.source == "synthetic":
+        return SyntheticSampler(cfg.cluster.dp, cfg.model.seq_len, cfg.model.vocab, cfg.run.seed)
+    from . import data as dt
+
+    return dt.ShardedSampler(n_ranks=cfg.cluster.dp, seq_len=cfg.model.seq_len, vocab_size=cfg.model.vocab,
+                             seed=cfg.run.seed, source=cfg.data.source, corpus_path=cfg.data.path)
+
+
 # ---------------------------------------------------------------------------
 # Crash-consistent writers (harness.py:167-201)
 # ---------------------------------------------------------------------------
@@ -240,7 +271,8 @@ def run_training(cfg: RunConfig, out_dir: str | None = None, quiet: bool = True,
                        tau=cfg.run.tau, optim_cfg=cfg.optimizer, weights=weights, svd=svd,
                        svd_budgeted=svd_budgeted)
     state = cl.ClusterState(cfg.cluster, cfg.scenario)
-    sampler = sampler or SyntheticSampler(n, cfg.model.seq_len, cfg.model.vocab, cfg.run.seed)
+    if sampler is None:
+        sampler = make_sampler(cfg)
     base_lr = cfg.run.base_lr if cfg.run.base_lr is not None else cfg.optimizer.lr
     metrics = AtomicFileWriter(os.path.join(out_dir, "metrics.csv") if out_dir else None, METRICS_HEADER)
     events_out = AtomicFileWriter(os.path.join(out_dir, "events.jsonl") if out_dir else None)
