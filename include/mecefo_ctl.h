@@ -29,6 +29,7 @@ extern "C" {
 
 #define MECEFO_CTL_OK 0
 #define MECEFO_CTL_CONTRACT 1
+#define MECEFO_CTL_UNRECOVERABLE 2
 
 typedef struct {
     uint64_t state_hi, state_lo; /* 128-bit LCG state */
@@ -51,6 +52,14 @@ int mecefo_pcg64_random(mecefo_pcg64_t* s, double* out, size_t count);
 
 /* Generator.integers(low, high, size=count) with int64 output, high > low. */
 int mecefo_pcg64_integers(mecefo_pcg64_t* s, int64_t low, int64_t high, int64_t* out, size_t count);
+
+/* Ring-successor takeover on one ring of n members (reference cluster.py:207-218,
+ * the NDB reassignment of reassign_takeover on one DP rank's stages): failed
+ * members in descending order each adopt the first following member that is
+ * neither failed nor already adopting. failed[j] != 0 marks member j;
+ * executor[j] receives the member that runs j's work (j itself if healthy).
+ * Returns MECEFO_CTL_UNRECOVERABLE when some failed member has no adopter. */
+int mecefo_ring_route(int32_t n, const uint8_t* failed, int32_t* executor);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,7 @@ from typing import Iterable
 import numpy as np
 
 from .errors import ConfigError, ConsistencyError, ContractViolation, UnrecoverableRankError
+from . import pcg as _pcg
 from .pcg import Pcg64Generator
 
 HEALTHY = "healthy"
@@ -243,20 +244,9 @@ def ring_route(n: int, failed) -> list | None:
     """Ring-successor takeover on one ring of n members (cluster.py:207-218):
     failed members in descending order each take the first following member
     that is neither failed nor already adopting. Returns executor[j] for every
-    member, or None if some failed member has no eligible adopter."""
-    failed = set(failed)
-    ex = list(range(n))
-    adopting = set()
-    for s in sorted(failed, reverse=True):
-        hop = 1
-        while hop < n and ((s + hop) % n in failed or (s + hop) % n in adopting):
-            hop += 1
-        if hop >= n:
-            return None
-        t = (s + hop) % n
-        adopting.add(t)
-        ex[s] = t
-    return ex
+    member, or None if some failed member has no eligible adopter. Runs in
+    the native control library (mecefo_ring_route, libmecefo_ctl.so)."""
+    return _pcg.ring_route(n, failed)
 
 
 def reassign_takeover(state: ClusterState, sim_time: float = 0.0, iteration: int = 0) -> list:

@@ -183,4 +183,32 @@ int mecefo_pcg64_integers(mecefo_pcg64_t* s, int64_t low, int64_t high, int64_t*
     return MECEFO_CTL_OK;
 }
 
+int mecefo_ring_route(int32_t n, const uint8_t* failed, int32_t* executor) {
+    if (n < 1 || !failed || !executor) return MECEFO_CTL_CONTRACT;
+    // adopting[t]: t already runs one failed member's work (one adoption each)
+    uint8_t stackbuf[256];
+    uint8_t* adopting = n <= 256 ? stackbuf : new uint8_t[n];
+    for (int32_t j = 0; j < n; ++j) {
+        adopting[j] = 0;
+        executor[j] = j;
+    }
+    int rc = MECEFO_CTL_OK;
+    for (int32_t s = n - 1; s >= 0 && rc == MECEFO_CTL_OK; --s) {
+        if (!failed[s]) continue;
+        int32_t hop = 1, t = (s + 1) % n;
+        while (hop < n && (failed[t] || adopting[t])) {
+            ++hop;
+            t = (s + hop) % n;
+        }
+        if (hop >= n) {
+            rc = MECEFO_CTL_UNRECOVERABLE;
+        } else {
+            adopting[t] = 1;
+            executor[s] = t;
+        }
+    }
+    if (adopting != stackbuf) delete[] adopting;
+    return rc;
+}
+
 }  // extern "C"

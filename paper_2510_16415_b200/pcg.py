@@ -5,7 +5,8 @@ streams of the host control plane.
 `np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy)))` for the
 calls the degraded-step control plane makes (reference
 pkg/src/faultsim/cluster.py:98,149,164; data.py:96,104): `random()` and
-`integers(low, high, size)`. There is no numpy fallback: a missing library
+`integers(low, high, size)`; plus the ring-successor takeover
+(`ring_route`, cluster.py:207-218). There is no numpy fallback: a missing library
 raises `EngineUnavailable`.
 """
 
@@ -29,7 +30,9 @@ SYMBOLS = {
     "mecefo_pcg64_next_u32": [ctypes.c_void_p, POINTER(c_uint32), c_size_t],
     "mecefo_pcg64_random": [ctypes.c_void_p, POINTER(c_double), c_size_t],
     "mecefo_pcg64_integers": [ctypes.c_void_p, c_int64, c_int64, POINTER(c_int64), c_size_t],
+    "mecefo_ring_route": [c_int32, POINTER(ctypes.c_uint8), POINTER(c_int32)],
 }
+MECEFO_CTL_UNRECOVERABLE = 2
 
 
 class _State(ctypes.Structure):
@@ -124,3 +127,18 @@ class Pcg64Generator:
                "mecefo_pcg64_next_u32")
         return out
 
+
+
+def ring_route(n: int, failed) -> list | None:
+    """mecefo_ring_route: executor list, or None when unrecoverable."""
+    if n < 1:
+        raise errors.ContractViolation(f"ring of {n} members")
+    mask = np.zeros(n, dtype=np.uint8)
+    for s in failed:
+        mask[int(s)] = 1
+    ex = np.empty(n, dtype=np.int32)
+    rc = load().mecefo_ring_route(n, mask.ctypes.data_as(POINTER(ctypes.c_uint8)), ex.ctypes.data_as(POINTER(c_int32)))
+    if rc == MECEFO_CTL_UNRECOVERABLE:
+        return None
+    _check(rc, "mecefo_ring_route")
+    return [int(v) for v in ex]
