@@ -44,6 +44,11 @@ C1 = dict(vocab=32000, hidden=512, heads=8, ffn=1376, layers=8, seq_len=256)
 SEQS = 32
 RANK = 128
 FAILED = (1,)
+# SURVEY.md §8 size table: C1 is the bench workload; C2-C4 dims via --model
+MODELS = {"60M": dict(vocab=32000, hidden=512, heads=8, ffn=1376, layers=8, seq_len=256),
+          "130M": dict(vocab=32000, hidden=768, heads=12, ffn=2048, layers=12, seq_len=256),
+          "350M": dict(vocab=32000, hidden=1024, heads=16, ffn=2736, layers=24, seq_len=256),
+          "1B": dict(vocab=32000, hidden=2048, heads=32, ffn=5472, layers=24, seq_len=256)}
 
 
 def _peaks():
@@ -195,7 +200,14 @@ def main():
     ap.add_argument("--no-fault-free", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--eager", action="store_true", help="launch kernels eagerly instead of CUDA-graph replay")
+    ap.add_argument("--model", default="60M", choices=sorted(MODELS),
+                    help="LLaMA dims (SURVEY.md §8 C1-C4); the bench workload is 60M (configs[1])")
     args = ap.parse_args()
+    if args.model != "60M":
+        global WORKLOAD
+        C1.update(MODELS[args.model])
+        WORKLOAD = (f"LLaMA-{args.model} synthetic seq 256, neighbour runs 2 microbatches with low-rank FFN grads "
+                    f"r=128 (SURVEY.md §8 dims; not the configs[1] bench workload)")
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -424,7 +436,7 @@ def main():
         "value_steady": round(value_steady, 1), "ms_per_step_steady": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision, "impl": "ours",
         "data": "synthetic (uniform tokens in [0,32000), PCG64 seeds 1000+j; weights = reference init_weights seed 0)",
-        "config": {"workload": WORKLOAD, "model": "LLaMA-60M", "global_batch": R * SEQS, "seq_len": cfg.seq_len,
+        "config": {"workload": WORKLOAD, "model": f"LLaMA-{args.model}", "global_batch": R * SEQS, "seq_len": cfg.seq_len,
                    "microbatch_tokens": b, "logical_ranks": R, "failed_ranks": list(FAILED), "rank_r": RANK,
                    "parallelism": f"dp{world} (MeCeFO ring, NDB neighbour)", "l2": "inputs larger than L2 "
                    "(per-step activations + logits > 126 MB)", "refresh_period": 100},
