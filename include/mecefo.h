@@ -48,6 +48,15 @@ enum {
 
 enum { MECEFO_PREC_F32 = 0, MECEFO_PREC_BF16 = 1 };
 
+/* Bits of the engine's device status word (sticky until reset). The kernels
+ * never read or write out of range on bad input: a token id outside
+ * [0, vocab) gathers a zero row and is skipped by the scatter-add, a bad
+ * target contributes loss 0 and a zero dlogits row. The host reads the word at
+ * iteration boundaries and raises what the reference raises:
+ *   BAD_TOKEN / BAD_TARGET -> ContractViolation (model.py:463, 505 IndexError)
+ *   NONFINITE_GRAD         -> NumericalFailure  (optim.py:55-57 _check_grad) */
+enum { MECEFO_STATUS_BAD_TOKEN = 1, MECEFO_STATUS_BAD_TARGET = 2, MECEFO_STATUS_NONFINITE_GRAD = 4 };
+
 /* model.py:30-31 CACHE_FULL / CACHE_FFN_INPUT_ONLY */
 enum { MECEFO_CACHE_FULL = 0, MECEFO_CACHE_FFN_INPUT_ONLY = 1 };
 
@@ -136,6 +145,15 @@ const char* mecefo_version(void);
 
 int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims);
 int mecefo_engine_destroy(mecefo_engine* e);
+/* Device pointer to the engine's int32 status word (MECEFO_STATUS_* bits);
+ * stream-ordered reset. */
+int mecefo_status_device(mecefo_engine* e, int32_t** device_status);
+int mecefo_status_reset(mecefo_engine* e, void* stream);
+/* Stream-ordered copy of the status word into (pinned) host memory; graph-capturable. */
+int mecefo_status_snapshot(mecefo_engine* e, int32_t* host_status, void* stream);
+/* Stream-ordered zero fill of a device range (gradient / loss accumulators). */
+int mecefo_memset_zero(void* device_ptr, size_t bytes, void* stream);
+
 /* Workspace bytes needed by any call below at `tokens` rows and padded rank. */
 size_t mecefo_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t rank_pad);
 
@@ -227,9 +245,12 @@ int mecefo_cast(mecefo_engine* e, const float* src, void* dst, int64_t n, void* 
 int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream);
 
 /* optim.py:96-103 apply_step with AdamW (optim.py:75-93) over a flat buffer;
- * skipped parameters are omitted from `segs`. `segs` is a DEVICE array.
- * shadow (optional) receives the updated weights in compute precision. */
-int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t nseg, int64_t max_numel, float* w,
+ * skipped parameters are omitted from `segs`. `segs` is a DEVICE array;
+ * total_numel = sum of the segments' numel (profiler byte count only).
+ * shadow (optional) receives the updated weights in compute precision.
+ * _check_grad (optim.py:55-57) is fused into the read of g: a non-finite
+ * gradient sets MECEFO_STATUS_NONFINITE_GRAD in the engine's status word. */
+int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t nseg, int64_t total_numel, float* w,
                       const float* grad, float* m, float* v, void* shadow, float beta1, float beta2, float eps,
                       void* stream);
 

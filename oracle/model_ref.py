@@ -17,6 +17,21 @@ LAYER_KINDS = ("q", "k", "v", "o", "norm_mha", "gate", "up", "down", "norm_ffn")
 FFN_KINDS = ("gate", "up", "down")  # approx.py:22
 
 
+def _mm_f64(a, b):
+    return np.matmul(a, b)
+
+
+# Every matrix product of the restatement goes through MM (BLAS-backed
+# np.matmul in float64). tests/golden/make_bf16_calibration.py swaps in a
+# PyTorch bf16 matmul to measure the error of a bf16-autocast implementation
+# of the same step; nothing else touches it.
+MM = _mm_f64
+
+
+def mm(a, b):
+    return MM(a, b)
+
+
 @dataclass(frozen=True)
 class Dims:
     vocab: int
@@ -105,10 +120,10 @@ def ffn_fwd(W, l, x1):
     """model.py:207-225 (== approx.recompute_ffn, approx.py:90-96)."""
     p = f"layers.{l}."
     h2, inv2 = rms_fwd(x1, W[p + "norm_ffn"])
-    gate = np.einsum("...m,fm->...f", h2, W[p + "gate"])
-    up = np.einsum("...m,fm->...f", h2, W[p + "up"])
+    gate = mm(h2, W[p + "gate"].T)
+    up = mm(h2, W[p + "up"].T)
     act = silu(gate) * up
-    down = np.einsum("...f,mf->...m", act, W[p + "down"])
+    down = mm(act, W[p + "down"].T)
     return dict(h2=h2, inv2=inv2, gate=gate, up=up, act=act, down=down)
 
 
@@ -118,14 +133,14 @@ def ffn_bwd(W, l, x1, it, dout, wgrad=None):
     n = int(np.prod(dout.shape[:-1]))
     flat = lambda a: a.reshape(n, a.shape[-1])
     if wgrad is None:
-        wgrad = lambda kind, d2, inp: d2.T @ inp
+        wgrad = lambda kind, d2, inp: mm(d2.T, inp)
     g = {"down": wgrad("down", flat(dout), flat(it["act"]))}
-    dact = np.einsum("...m,mf->...f", dout, W[p + "down"])
+    dact = mm(dout, W[p + "down"])
     dup = dact * silu(it["gate"])
     dgate = dact * it["up"] * dsilu(it["gate"])
     g["gate"] = wgrad("gate", flat(dgate), flat(it["h2"]))
     g["up"] = wgrad("up", flat(dup), flat(it["h2"]))
-    dh2 = np.einsum("...f,fm->...m", dgate, W[p + "gate"]) + np.einsum("...f,fm->...m", dup, W[p + "up"])
+    dh2 = mm(dgate, W[p + "gate"]) + mm(dup, W[p + "up"])
     dx1, g["norm_ffn"] = rms_bwd(x1, W[p + "norm_ffn"], it["inv2"], dh2)
     return dx1, {k: g[k] for k in ("gate", "up", "down", "norm_ffn")}
 
@@ -160,20 +175,20 @@ def heads_merge(x):
 def attn_fwd(d: Dims, W, l, h1):
     """model.py:317-333."""
     p = f"layers.{l}."
-    q = heads_split(h1 @ W[p + "q"].T, d.heads)
-    k = heads_split(h1 @ W[p + "k"].T, d.heads)
-    v = heads_split(h1 @ W[p + "v"].T, d.heads)
+    q = heads_split(mm(h1, W[p + "q"].T), d.heads)
+    k = heads_split(mm(h1, W[p + "k"].T), d.heads)
+    v = heads_split(mm(h1, W[p + "v"].T), d.heads)
     T = h1.shape[1]
     if d.rope:
         c, s = rope_tables(T, d.hd)
         q, k = rope(q, c, s), rope(k, c, s)
-    sc = np.einsum("bhid,bhjd->bhij", q, k) / math.sqrt(d.hd)
+    sc = mm(q, k.swapaxes(-1, -2)) / math.sqrt(d.hd)
     sc = np.where(np.triu(np.ones((T, T), bool), 1), -np.inf, sc)
     sc = sc - sc.max(-1, keepdims=True)
     pr = np.exp(sc)
     pr /= pr.sum(-1, keepdims=True)
-    ctx = heads_merge(np.einsum("bhij,bhjd->bhid", pr, v))
-    return dict(q=q, k=k, v=v, probs=pr, ctx=ctx, out=ctx @ W[p + "o"].T)
+    ctx = heads_merge(mm(pr, v))
+    return dict(q=q, k=k, v=v, probs=pr, ctx=ctx, out=mm(ctx, W[p + "o"].T))
 
 
 def attn_bwd(d: Dims, W, l, h1, a, dout):
@@ -181,22 +196,22 @@ def attn_bwd(d: Dims, W, l, h1, a, dout):
     p = f"layers.{l}."
     B, T, m = h1.shape
     n = B * T
-    g = {"o": dout.reshape(n, m).T @ a["ctx"].reshape(n, m)}
-    dctx = heads_split(dout @ W[p + "o"], d.heads)
+    g = {"o": mm(dout.reshape(n, m).T, a["ctx"].reshape(n, m))}
+    dctx = heads_split(mm(dout, W[p + "o"]), d.heads)
     pr = a["probs"]
-    dpr = np.einsum("bhid,bhjd->bhij", dctx, a["v"])
-    dv = np.einsum("bhij,bhid->bhjd", pr, dctx)
+    dpr = mm(dctx, a["v"].swapaxes(-1, -2))
+    dv = mm(pr.swapaxes(-1, -2), dctx)
     ds = pr * (dpr - (dpr * pr).sum(-1, keepdims=True))
     sc = 1.0 / math.sqrt(d.hd)
-    dq = np.einsum("bhij,bhjd->bhid", ds, a["k"]) * sc
-    dk = np.einsum("bhij,bhid->bhjd", ds, a["q"]) * sc
+    dq = mm(ds, a["k"]) * sc
+    dk = mm(ds.swapaxes(-1, -2), a["q"]) * sc
     if d.rope:
         c, s = rope_tables(T, d.hd)
         dq, dk = rope(dq, c, s, inverse=True), rope(dk, c, s, inverse=True)
     mq, mk, mv = (heads_merge(t).reshape(n, m) for t in (dq, dk, dv))
     h = h1.reshape(n, m)
-    g["q"], g["k"], g["v"] = mq.T @ h, mk.T @ h, mv.T @ h
-    dh1 = (mq @ W[p + "q"] + mk @ W[p + "k"] + mv @ W[p + "v"]).reshape(B, T, m)
+    g["q"], g["k"], g["v"] = mm(mq.T, h), mm(mk.T, h), mm(mv.T, h)
+    dh1 = (mm(mq, W[p + "q"]) + mm(mk, W[p + "k"]) + mm(mv, W[p + "v"])).reshape(B, T, m)
     return dh1, g
 
 
@@ -227,7 +242,7 @@ def block_bwd_exact(d: Dims, W, l, cache, dy):
 
 def lowrank(g_y, x, v1):
     """approx.py:24-42: g_y (x^T v1) v1^T in exactly that association order."""
-    return (g_y @ (x.T @ v1)) @ v1.T
+    return mm(mm(g_y, mm(x.T, v1)), v1.T)
 
 
 def block_bwd_neighbor(d: Dims, W, l, cache, dy, basis=None):
@@ -285,10 +300,10 @@ def rank_pass(d: Dims, W, tokens, targets, modes, bases=None):
         caches.append(c)
     xf, invf = rms_fwd(x, W["final_norm"])
     xf2 = xf.reshape(-1, d.hidden)
-    logits = xf2 @ W["unembedding"].T
+    logits = mm(xf2, W["unembedding"].T)
     loss, dl = cross_entropy(logits, targets)
-    g = {"unembedding": dl.T @ xf2}
-    dx, g["final_norm"] = rms_bwd(x, W["final_norm"], invf, (dl @ W["unembedding"]).reshape(x.shape))
+    g = {"unembedding": mm(dl.T, xf2)}
+    dx, g["final_norm"] = rms_bwd(x, W["final_norm"], invf, mm(dl, W["unembedding"]).reshape(x.shape))
     for l in reversed(range(d.layers)):
         if modes[l] == "full":
             dx, gl = block_bwd_exact(d, W, l, caches[l], dx)

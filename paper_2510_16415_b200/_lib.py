@@ -21,6 +21,9 @@ PREC_F32 = 0
 PREC_BF16 = 1
 CACHE_FULL = 0
 CACHE_FFN_INPUT_ONLY = 1
+STATUS_BAD_TOKEN = 1
+STATUS_BAD_TARGET = 2
+STATUS_NONFINITE_GRAD = 4
 
 
 class EngineUnavailable(RuntimeError):
@@ -143,6 +146,10 @@ _SIGNATURES = {
     "mecefo_engine_create": (c_int, [POINTER(c_void_p), POINTER(Dims)]),
     "mecefo_engine_destroy": (c_int, [c_void_p]),
     "mecefo_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32]),
+    "mecefo_status_device": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "mecefo_status_reset": (c_int, [c_void_p, c_void_p]),
+    "mecefo_status_snapshot": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mecefo_memset_zero": (c_int, [c_void_p, c_size_t, c_void_p]),
     "mecefo_forward_block": (
         c_int,
         [c_void_p, POINTER(LayerWeights), POINTER(BlockCache), c_void_p, c_void_p, c_int64, c_int32, c_void_p,

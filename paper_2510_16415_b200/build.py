@@ -14,12 +14,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libmecefo.so")
-SOURCES = ["engine.cu"]
-DEPS = ["common.cuh", "gemm.cuh", "kernels.cuh", "attention.cuh", "attention_tc.cuh", "attention_bwd_tc.cuh", "gemm_dual.cuh", "subspace.cuh", "ce.cuh", "engine.cu"]
+SOURCES = ["engine.cu", "refresh.cu"]
+DEPS = ["common.cuh", "host.h", "gemm.cuh", "kernels.cuh", "attention.cuh", "attention_tc.cuh", "attention_bwd_tc.cuh",
+        "gemm_dual.cuh", "subspace.cuh", "ce.cuh", "refresh.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-I", os.path.join(ROOT, "include"),
 ]
 
@@ -35,7 +36,8 @@ def stale() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    files = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(ROOT, "include", "mecefo.h")]
+    files = [os.path.join(CSRC, d) for d in DEPS + SOURCES if os.path.exists(os.path.join(CSRC, d))] + \
+        [os.path.join(ROOT, "include", "mecefo.h")]
     return any(os.path.getmtime(f) > t for f in files)
 
 
@@ -61,11 +63,25 @@ def build(force: bool = False, verbose: bool = True) -> str:
     build_control(force, verbose)
     if not force and not stale():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    # one translation unit per .cu, compiled in parallel, then linked
+    objs, procs = [], []
+    for src in [x for x in SOURCES if os.path.exists(os.path.join(CSRC, x))]:
+        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print("[build]", " ".join(cmd), flush=True)
+        procs.append(subprocess.Popen(cmd))
+        objs.append(obj)
+    rcs = [p.wait() for p in procs]
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), "nvcc")
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT + ".tmp", *objs]
     if verbose:
         print("[build]", " ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)
+    for o in objs:
+        os.remove(o)
     return OUT
 
 

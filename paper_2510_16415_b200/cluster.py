@@ -312,9 +312,13 @@ def active_set(state: ClusterState, layer: int, kind: str) -> list:
 
 
 def aggregate_gradients(per_rank: list, active: dict, layers: int):
-    """cluster.py:292-322 on device tensors: ascending-rank accumulation of
-    g_i / |N|; empty active sets are skipped (never multiplied, so values on
-    excluded ranks cannot leak); missing gradients raise ConsistencyError."""
+    """cluster.py:292-322 on the device: per-rank gradients (torch tensors or
+    the reference's numpy arrays) -> fp32 CUDA averages, ascending-rank
+    accumulation of g_i / |N|; empty active sets are skipped (excluded ranks
+    are never read, so non-finite values there cannot leak); missing
+    gradients raise ConsistencyError."""
+    import torch
+
     from . import _lib, runtime
 
     n = len(per_rank)
@@ -324,14 +328,14 @@ def aggregate_gradients(per_rank: list, active: dict, layers: int):
         for i in ranks:
             if name not in per_rank[i]:
                 raise ConsistencyError(f"rank {i} is missing gradient {name!r}")
-        first = per_rank[ranks[0]][name]
-        out = first.detach().to(dtype=first.dtype).contiguous().float().clone()
         k = 1.0 / len(ranks)
-        _lib.call("mecefo_scale_accumulate", out.data_ptr(), out.data_ptr(), out.numel(), k, 0.0,
-                  runtime.stream_ptr())
-        for i in ranks[1:]:
-            g = per_rank[i][name].detach().float().contiguous()
-            _lib.call("mecefo_scale_accumulate", g.data_ptr(), out.data_ptr(), out.numel(), k, 1.0,
+        grads = [torch.as_tensor(per_rank[i][name]).detach().to("cuda", torch.float32).contiguous() for i in ranks]
+        out = torch.zeros_like(grads[0])
+        for g in grads:  # ascending rank order; out += g / |N| (never aliased)
+            if tuple(g.shape) != tuple(out.shape):
+                raise ConsistencyError(f"gradient {name!r} has shape {tuple(g.shape)} on one rank, "
+                                       f"{tuple(out.shape)} on another")
+            _lib.call("mecefo_scale_accumulate", runtime.ptr(g), runtime.ptr(out), out.numel(), k, 1.0,
                       runtime.stream_ptr())
         return out
 

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_wait(&bars[cur], NB == 2 ? ((it >> 1) & 1) : (it & 1));
     const int64_t t = targets[r];
     const bool tgt_ok = t >= 0 && t < V;
-    if (!tgt_ok && tid == 0) atomicExch(bad_target, 1);
+    if (!tgt_ok && tid == 0) atomicOr(bad_target, 2);
     const uint8_t* bufc = ces_smem + cur * rb_al;
     const uint4* sv = reinterpret_cast<const uint4*>(bufc);
     // pass 1 (smem): per-thread online (max, sum exp)
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(NT, 1)
       for (int j = 0; j < 4; ++j) {
         const float2 q = __bfloat1622float2(h[j]);
         const float2 e2 = ex2_h2(fmaf(q.x, 1.4426950408889634f, -mxl), fmaf(q.y, 1.4426950408889634f, -mxl));
-        float p0 = e2.x * sc, p1 = e2.y * sc;
+        float p0 = tgt_ok ? e2.x * sc : 0.f, p1 = tgt_ok ? e2.y * sc : 0.f;  // invalid target: zero row
         const int c = vi * 8 + 2 * j;
         if (c == t) p0 -= inv_n;
         if (c + 1 == t) p1 -= inv_n;

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -17,6 +18,7 @@
 #include <utility>
 
 #include "../../include/mecefo.h"
+#include "host.h"
 #include "attention.cuh"
 #include "attention_tc.cuh"
 #include "attention_bwd_tc.cuh"
@@ -27,44 +29,14 @@
 #include "ce.cuh"
 
 using namespace mecefo;
+using namespace mecefo_host;
 
 // ---------------------------------------------------------------------------
-// errors
+// errors, launch counter, launch profiler (shared with refresh.cu via host.h)
 // ---------------------------------------------------------------------------
 namespace {
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
-
-int set_err(int code, const char* fmt, ...) {
-  char buf[1024];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
-  g_last_error = buf;
-  return code;
-}
-
-#define CUDA_TRY(expr)                                                                          \
-  do {                                                                                          \
-    cudaError_t _e = (expr);                                                                    \
-    if (_e != cudaSuccess)                                                                      \
-      return set_err(MECEFO_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
-                     __FILE__, __LINE__);                                                       \
-  } while (0)
-
-#define TRY(expr)               \
-  do {                          \
-    int _rc = (expr);           \
-    if (_rc != MECEFO_OK) return _rc; \
-  } while (0)
-
-int check_launch(const char* what) {
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(MECEFO_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
-  return MECEFO_OK;
-}
 
 // Optional launch profiler: CUDA events around each kernel (or fused
 // kernel group) tagged with its algorithmic FLOPs and HBM bytes. Enabled by
@@ -90,48 +62,65 @@ struct Profiler {
 };
 Profiler g_prof;
 std::mutex g_prof_mu;
+}  // namespace
 
-struct ProfScope {
-  int64_t idx = -1;
-  cudaStream_t s;
-  ProfScope(const char* tag, double flops, double bytes, cudaStream_t st) : s(st) {
-    if (!g_prof.on) return;
-    std::lock_guard<std::mutex> lk(g_prof_mu);
-    g_prof.recs.push_back(ProfRec{tag, g_prof.ev(), g_prof.ev(), flops, bytes});
-    idx = (int64_t)g_prof.recs.size() - 1;
-    cudaEventRecord(g_prof.recs[idx].a, s);
-  }
-  ~ProfScope() {
-    if (idx < 0) return;
-    std::lock_guard<std::mutex> lk(g_prof_mu);
-    if (idx < (int64_t)g_prof.recs.size()) cudaEventRecord(g_prof.recs[idx].b, s);
-  }
-};
+namespace mecefo_host {
 
-// Every engine kernel goes out with programmatic stream serialization (PDL):
-// it may be scheduled while its predecessor drains, runs its prologue
-// (barrier init, TMEM alloc, descriptor prefetch) and blocks in
-// griddepcontrol.wait until the predecessor's results are visible. Kept in
-// CUDA-graph capture as programmatic edges. MECEFO_NO_PDL=1 disables it.
+int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(MECEFO_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+  return MECEFO_OK;
+}
+
+int64_t prof_begin(const char* tag, double flops, double bytes, cudaStream_t s) {
+  if (!g_prof.on) return -1;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.recs.push_back(ProfRec{tag, g_prof.ev(), g_prof.ev(), flops, bytes});
+  const int64_t idx = (int64_t)g_prof.recs.size() - 1;
+  cudaEventRecord(g_prof.recs[idx].a, s);
+  return idx;
+}
+
+void prof_end(int64_t idx, cudaStream_t s) {
+  if (idx < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (idx < (int64_t)g_prof.recs.size()) cudaEventRecord(g_prof.recs[idx].b, s);
+}
+
 bool pdl_enabled() {
   static const bool on = getenv("MECEFO_NO_PDL") == nullptr;
   return on;
 }
 
-template <typename... KArgs, typename... Args>
-cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+// Dynamic shared memory opt-in per (kernel, device): a process that drives
+// several GPUs configures each device's copy of the kernel once.
+int ensure_smem(const void* kern, int bytes) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find({kern, dev});
+  if (it != done.end() && it->second >= bytes) return MECEFO_OK;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[{kern, dev}] = bytes;
+  return MECEFO_OK;
 }
+
+}  // namespace mecefo_host
+
+namespace {
 
 // Bump allocator over the caller's workspace.
 struct Ws {
@@ -187,6 +176,10 @@ struct mecefo_engine {
   int ps;  // bytes per compute-precision element
   float* rope_cos = nullptr;
   float* rope_sin = nullptr;
+  // device status word (bits MECEFO_STATUS_*): bad token / bad target /
+  // non-finite gradient, set by the kernels, read by the host at iteration
+  // boundaries (model.py:463 IndexError, optim.py:55-57 _check_grad)
+  int* status = nullptr;
   std::mutex mu;
   std::unordered_map<TmKey, CUtensorMap, TmHash> tmaps;
 };
@@ -345,20 +338,15 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   // fp32 residual boxes (same 32x32 SW128 layout as the fp32 store)
   if (ep.kind == EPI_STORE && ep.residual && outs.used[0] && outs.prec[0] == PREC_F32 && !g.paired)
     TRY(make_tmap(e, &mp.r, ep.residual, g.N, g.M, ep.ldr, 32, 32, 1, 128));
-  {  // timing experiments only: MECEFO_DBG_NOEPI drops every output, MECEFO_DBG_NOROPE the rotation
-    static const bool no_epi = getenv("MECEFO_DBG_NOEPI") != nullptr;
-    static const bool no_rope = getenv("MECEFO_DBG_NOROPE") != nullptr;
-    if (no_epi) outs.used[0] = outs.used[1] = outs.used[2] = 0;
-    if (no_rope) p.epi.rope_cos = nullptr;
-    static const bool no_res = getenv("MECEFO_DBG_NORES") != nullptr;
-    if (no_res) p.epi.residual = nullptr;
+#ifdef MECEFO_TIMING_KNOBS
+  {  // timing experiments only (never in a product build): drop outputs / rotation / residual
+    if (getenv("MECEFO_DBG_NOEPI")) outs.used[0] = outs.used[1] = outs.used[2] = 0;
+    if (getenv("MECEFO_DBG_NOROPE")) p.epi.rope_cos = nullptr;
+    if (getenv("MECEFO_DBG_NORES")) p.epi.residual = nullptr;
   }
+#endif
   auto kern = gemm_tc_kernel<BN, AK, BKM, CL, NG, ROPE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
-  }
+  TRY(ensure_smem((const void*)kern, C::SMEM));
   const int grid = CL * std::min(p.num_tiles_cl, kNumSMs / CL);
   if (CL == 1) {
     CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, mp, p, outs));
@@ -542,11 +530,7 @@ template <int NV>
 int launch_rms_bwd(const float* x, const float* g, const float* inv, const float* d, const float* resid, float* dx,
                    void* dx_lp, int prec, float* partial, int64_t rows, int64_t m, int nblk, int rpb, cudaStream_t s) {
   const int sm = 8 * NV * 32 * 16;
-  static bool set = false;
-  if (!set && sm > 48 * 1024) {
-    CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_vec_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    set = true;
-  }
+  if (sm > 48 * 1024) TRY(ensure_smem((const void*)rmsnorm_bwd_vec_kernel<NV>, sm));
   CUDA_TRY(pdl_launch(rmsnorm_bwd_vec_kernel<NV>, dim3(nblk), dim3(256), sm, s, x, g, inv, d, resid, dx, dx_lp, prec, partial, (int)rows, (int)m,
                                                    rpb));
   return check_launch("rmsnorm_bwd_vec_kernel");
@@ -582,8 +566,7 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
   } else {
     const size_t sm = 8 * m * sizeof(float);
     if (sm > 48 * 1024) {
-      static bool set = false;
-      if (!set) { CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); set = true; }
+      TRY(ensure_smem((const void*)rmsnorm_bwd_kernel, 200 * 1024));
     }
     CUDA_TRY(pdl_launch(rmsnorm_bwd_kernel, dim3(nblk), dim3(256), sm, s, x, g, inv, d, resid, dx, dx_lp, e->prec, partial, (int)rows, (int)m, rpb));
     TRY(check_launch("rmsnorm_bwd_kernel"));
@@ -619,11 +602,7 @@ int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const vo
   p.tiles_n = (int)((f + D2_NP - 1) / D2_NP);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.has_act = act ? 1 : 0;
-  static bool set128 = false;
-  if (!set128) {
-    CUDA_TRY(cudaFuncSetAttribute(swiglu_bwd_dual128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D2_SMEM));
-    set128 = true;
-  }
+  TRY(ensure_smem((const void*)swiglu_bwd_dual128_kernel, D2_SMEM));
   CUDA_TRY(pdl_launch(swiglu_bwd_dual128_kernel, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), D2_SMEM, s,
                       tdy, th2, twd, twgu128, tact, tdg, tdu, p));
   return check_launch("swiglu_bwd_dual128_kernel");
@@ -642,11 +621,7 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
     CUtensorMap tq;
     TRY(make_tmap(e, &tq, a.qkv, 3 * a.m, tokens, a.ld_qkv, 64, 64));
     AttnTcArgs t{a.ctx, a.ld_ctx, a.lse, a.T, a.H, a.m, a.scale};
-    static bool set = false;
-    if (!set) {
-      CUDA_TRY(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATC_SMEM));
-      set = true;
-    }
+    TRY(ensure_smem((const void*)attn_fwd_tc_kernel, ATC_SMEM));
     dim3 grid((unsigned)(tokens / a.T) * a.H, (unsigned)((a.T + 127) / 128));
     CUDA_TRY(pdl_launch(attn_fwd_tc_kernel, dim3(grid), dim3(ATC_THREADS), ATC_SMEM, s, tq, t));
     return check_launch("attn_fwd_tc_kernel");
@@ -657,11 +632,7 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
     TRY(make_tmap(e, &tq, a.qkv, 3 * a.m, tokens, a.ld_qkv, 64, 64));
     TRY(make_tmap(e, &tdo, a.dctx, a.m, tokens, a.ld_ctx, 64, 64));
     AttnBwdTcArgs t{a.ctx, a.dctx, a.lse, a.dqkv, a.cosT, a.sinT, a.T, a.H, a.m, a.rope, a.scale};
-    static bool set = false;
-    if (!set) {
-      CUDA_TRY(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ABT_SMEM));
-      set = true;
-    }
+    TRY(ensure_smem((const void*)attn_bwd_tc_kernel, ABT_SMEM));
     CUDA_TRY(pdl_launch(attn_bwd_tc_kernel, dim3((unsigned)((tokens / a.T) * a.H)), dim3(ABT_THREADS), ABT_SMEM, s, tq, tdo, t));
     return check_launch("attn_bwd_tc_kernel");
   }
@@ -790,9 +761,12 @@ int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims) {
   if (ce == cudaSuccess) ce = cudaMalloc(&e->rope_sin, sn.size() * sizeof(float));
   if (ce == cudaSuccess) ce = cudaMemcpy(e->rope_cos, c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (ce == cudaSuccess) ce = cudaMemcpy(e->rope_sin, sn.data(), sn.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMalloc(&e->status, 16);
+  if (ce == cudaSuccess) ce = cudaMemset(e->status, 0, 16);
   if (ce != cudaSuccess) {
     cudaFree(e->rope_cos);
     cudaFree(e->rope_sin);
+    cudaFree(e->status);
     delete e;
     return set_err(MECEFO_ERR_CUDA, "engine allocation failed: %s", cudaGetErrorString(ce));
   }
@@ -804,7 +778,32 @@ int mecefo_engine_destroy(mecefo_engine* e) {
   if (!e) return MECEFO_OK;
   cudaFree(e->rope_cos);
   cudaFree(e->rope_sin);
+  cudaFree(e->status);
   delete e;
+  return MECEFO_OK;
+}
+
+int mecefo_status_device(mecefo_engine* e, int32_t** out) {
+  if (!e || !out) return set_err(MECEFO_ERR_CONTRACT, "null argument");
+  *out = e->status;
+  return MECEFO_OK;
+}
+
+int mecefo_status_snapshot(mecefo_engine* e, int32_t* host, void* stream) {
+  if (!e || !host) return set_err(MECEFO_ERR_CONTRACT, "null argument");
+  CUDA_TRY(cudaMemcpyAsync(host, e->status, 4, cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)));
+  return MECEFO_OK;
+}
+
+int mecefo_memset_zero(void* p, size_t bytes, void* stream) {
+  if (bytes == 0) return MECEFO_OK;
+  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, reinterpret_cast<cudaStream_t>(stream)));
+  return MECEFO_OK;
+}
+
+int mecefo_status_reset(mecefo_engine* e, void* stream) {
+  if (!e) return set_err(MECEFO_ERR_CONTRACT, "null engine");
+  CUDA_TRY(cudaMemsetAsync(e->status, 0, 16, reinterpret_cast<cudaStream_t>(stream)));
   return MECEFO_OK;
 }
 
@@ -1364,7 +1363,8 @@ int mecefo_embedding_forward(mecefo_engine* e, const int64_t* tokens, const floa
                              void* stream) {
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if (n <= 0) return MECEFO_OK;
-  CUDA_TRY(pdl_launch(embedding_fwd_kernel, dim3((unsigned)n), dim3(128), 0, s, tokens, emb, x, (int)n, (int)e->d.hidden));
+  CUDA_TRY(pdl_launch(embedding_fwd_kernel, dim3((unsigned)n), dim3(128), 0, s, tokens, emb, x, (int)n, (int)e->d.hidden,
+                      (int)e->d.vocab, e->status));
   return check_launch("embedding_fwd_kernel");
 }
 
@@ -1391,10 +1391,8 @@ int mecefo_cross_entropy_grouped(mecefo_engine* e, void* logits, const int64_t* 
   const float inv_n = 1.f / (float)group_rows;
   Ws ws(wsp, ws_bytes);
   float* rows;
-  int* bad;
+  int* bad = e->status;  // bit MECEFO_STATUS_BAD_TARGET; the row contributes loss 0 and zero dlogits
   TRY(ws.take(b * 4, reinterpret_cast<void**>(&rows)));
-  TRY(ws.take(16, reinterpret_cast<void**>(&bad)));
-  CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
   ProfScope prof("cross_entropy", 0.0, 2.0 * b * V * e->ps, s);
   // bf16: a row per CTA staged in shared memory (read once, written once),
   // several CTAs per SM; f16x2 exps (cross_entropy_smem_kernel, ce.cuh).
@@ -1402,12 +1400,7 @@ int mecefo_cross_entropy_grouped(mecefo_engine* e, void* logits, const int64_t* 
   const size_t rb_al = ((size_t)V * 2 + 127) & ~size_t(127);
   const size_t ce_smem = rb_al + 16 + 8 * 32 + 128;
   if (e->prec == PREC_BF16 && V % 8 == 0 && ce_smem <= 200 * 1024) {
-    static bool cfg = false;
-    if (!cfg) {
-      CUDA_TRY(cudaFuncSetAttribute(cross_entropy_smem_kernel<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
-      cfg = true;
-    }
+    TRY(ensure_smem((const void*)cross_entropy_smem_kernel<1, 256>, 200 * 1024));
     const int per_sm = std::max(1, (int)((220 * 1024) / (ce_smem + 1024)));
     CUDA_TRY(pdl_launch(cross_entropy_smem_kernel<1, 256>, dim3((unsigned)std::min<int64_t>(b, kNumSMs * per_sm)),
                         dim3(256), ce_smem, s, reinterpret_cast<__nv_bfloat16*>(logits), V, targets, rows, (int)b,
@@ -1481,7 +1474,8 @@ int mecefo_embedding_backward(mecefo_engine* e, const int64_t* tokens, const flo
                               int64_t n, void* stream) {
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if (n <= 0) return MECEFO_OK;
-  CUDA_TRY(pdl_launch(embedding_bwd_kernel, dim3((unsigned)n), dim3(128), 0, s, tokens, dx0, g_emb, (int)n, (int)e->d.hidden, alpha));
+  CUDA_TRY(pdl_launch(embedding_bwd_kernel, dim3((unsigned)n), dim3(128), 0, s, tokens, dx0, g_emb, (int)n, (int)e->d.hidden, alpha,
+                      (int)e->d.vocab));
   return check_launch("embedding_bwd_kernel");
 }
 
@@ -1504,18 +1498,18 @@ int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream) {
   return check_launch("nonfinite_kernel");
 }
 
-int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t nseg, int64_t max_numel, float* w,
+int mecefo_adamw_step(mecefo_engine* e, const mecefo_adam_segment* segs, int32_t nseg, int64_t total_numel, float* w,
                       const float* grad, float* m1, float* m2, void* shadow, float beta1, float beta2, float eps,
                       void* stream) {
   if (nseg <= 0) return MECEFO_OK;
   static_assert(sizeof(mecefo_adam_segment) == sizeof(AdamSeg), "segment layout");
-  (void)max_numel;
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  ProfScope prof("adamw", 0.0, 0.0, s);
+  // read g, m, v, w; write m, v, w (+ the compute-precision shadow)
+  ProfScope prof("adamw", 0.0, (double)total_numel * (28.0 + (shadow ? (e ? e->ps : 4) : 0)), s);
   const unsigned grid = 8 * kNumSMs;  // grid-stride over the concatenated active segments
   CUDA_TRY(pdl_launch(adamw_kernel, dim3(grid), dim3(256), (nseg + 1) * sizeof(int64_t), s, reinterpret_cast<const AdamSeg*>(segs), nseg, w, grad,
                                                                m1, m2, shadow, e ? e->prec : PREC_F32, beta1, beta2,
-                                                               eps));
+                                                               eps, e ? e->status : nullptr));
   return check_launch("adamw_kernel");
 }
 
@@ -1801,14 +1795,8 @@ int mecefo_subspace_iteration_batched(mecefo_engine* e, const mecefo_subspace_jo
   // pageable sources: the copies are staged before these calls return
   CUDA_TRY(cudaMemcpyAsync(dj, hj.data(), hj.size() * sizeof(SubGemmJob), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(dk, hk.data(), hk.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-  static bool configured = false;
-  if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(subspace_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SUB_SMEM_MAX));
-    CUDA_TRY(cudaFuncSetAttribute(subspace_ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SUB_SMEM_MAX));
-    configured = true;
-  }
+  TRY(ensure_smem((const void*)subspace_chol_inv_kernel, (int)SUB_SMEM_MAX));
+  TRY(ensure_smem((const void*)subspace_ritz_kernel, (int)SUB_SMEM_MAX));
   void* scratch = p.smem ? nullptr : ws + p.off_scr;
   const size_t scr_stride = std::max(p.chol_bytes, p.ritz_bytes);
   static const char* const phase_tag[SUB_PHASES] = {"subspace.gram_w", "subspace.bv", "subspace.gram_z",

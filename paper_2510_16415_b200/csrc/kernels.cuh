@@ -125,22 +125,33 @@ __global__ void colsum_finalize_kernel(const float* __restrict__ partial, int nb
 // ---------------------------------------------------------------------------
 // Embedding gather / scatter-add (model.py:463, 486-489).
 // ---------------------------------------------------------------------------
+// Token ids outside [0, vocab) (the reference raises IndexError on the gather,
+// model.py:463) never touch memory out of range: the gather writes a zero row
+// and sets status[MECEFO_STATUS_BAD_TOKEN]; the scatter-add skips the row.
 __global__ void embedding_fwd_kernel(const int64_t* __restrict__ tok, const float* __restrict__ emb,
-                                     float* __restrict__ out, int rows, int m) {
+                                     float* __restrict__ out, int rows, int m, int vocab, int* __restrict__ status) {
   griddep_wait();
   const int row = blockIdx.x;
   if (row >= rows) return;
-  const float* e = emb + tok[row] * (int64_t)m;
+  const int64_t t = tok[row];
   float* o = out + (int64_t)row * m;
+  if (t < 0 || t >= vocab) {
+    if (threadIdx.x == 0 && status) atomicOr(status, 1);
+    for (int c = threadIdx.x; c < m; c += blockDim.x) o[c] = 0.f;
+    return;
+  }
+  const float* e = emb + t * (int64_t)m;
   for (int c = threadIdx.x; c < m; c += blockDim.x) o[c] = e[c];
 }
 
 __global__ void embedding_bwd_kernel(const int64_t* __restrict__ tok, const float* __restrict__ dx,
-                                     float* __restrict__ grad, int rows, int m, float alpha) {
+                                     float* __restrict__ grad, int rows, int m, float alpha, int vocab) {
   griddep_wait();
   const int row = blockIdx.x;
   if (row >= rows) return;
-  float* gp = grad + tok[row] * (int64_t)m;
+  const int64_t t = tok[row];
+  if (t < 0 || t >= vocab) return;
+  float* gp = grad + t * (int64_t)m;
   const float* d = dx + (int64_t)row * m;
   for (int c = threadIdx.x; c < m; c += blockDim.x) atomicAdd(gp + c, alpha * d[c]);
 }
@@ -166,8 +177,12 @@ __global__ void cross_entropy_kernel(void* __restrict__ logits, int64_t ld, cons
   s = block_sum(s, red);
   const float lse = mx + logf(s);
   const int64_t t = targets[row];
-  if (t < 0 || t >= V) {
-    if (threadIdx.x == 0) atomicExch(bad_target, 1);
+  if (t < 0 || t >= V) {  // model.py:505 would raise IndexError: flag it, contribute nothing
+    if (threadIdx.x == 0) {
+      atomicOr(bad_target, 2);
+      loss_rows[row] = 0.f;
+    }
+    for (int c = threadIdx.x; c < V; c += blockDim.x) store_from_f32(logits, base + c, 0.f, prec);
     return;
   }
   const float zt = load_as_f32(logits, base + t, prec);
@@ -265,7 +280,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(const AdamSeg* __restrict__ 
                                                     float* __restrict__ w, const float* __restrict__ grad,
                                                     float* __restrict__ m1, float* __restrict__ m2,
                                                     void* __restrict__ shadow, int shadow_prec, float beta1,
-                                                    float beta2, float eps) {
+                                                    float beta2, float eps, int* __restrict__ status) {
   griddep_wait();
   extern __shared__ int64_t cum[];  // nseg + 1 prefix sums of numel
   if (threadIdx.x == 0) {
@@ -278,8 +293,13 @@ __global__ void __launch_bounds__(256) adamw_kernel(const AdamSeg* __restrict__ 
   }
   __syncthreads();
   const int64_t total = cum[nseg];
+  // optim.py:55-57 _check_grad, fused into the read of g: any non-finite
+  // gradient sets status[MECEFO_STATUS_NONFINITE_GRAD] (read by the host at the
+  // iteration boundary, which raises NumericalFailure)
+  bool bad = false;
   auto upd = [&](const AdamSeg& sg, int64_t i) {
     const float g = grad[i];
+    bad |= !isfinite(g);
     float mm = m1[i], vv = m2[i];
     mm = beta1 * mm + (1.f - beta1) * g;
     vv = beta2 * vv + (1.f - beta2) * (g * g);
@@ -304,6 +324,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(const AdamSeg* __restrict__ 
       float4 mm = *reinterpret_cast<const float4*>(m1 + i), vv = *reinterpret_cast<const float4*>(m2 + i);
       float4 wi = *reinterpret_cast<const float4*>(w + i);
       float gg[4] = {g.x, g.y, g.z, g.w}, ma[4] = {mm.x, mm.y, mm.z, mm.w}, va[4] = {vv.x, vv.y, vv.z, vv.w};
+      bad |= !(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w));
       float wa[4] = {wi.x, wi.y, wi.z, wi.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -333,6 +354,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(const AdamSeg* __restrict__ 
       }
     }
   }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && status) atomicOr(status, 4);
 }
 
 }  // namespace mecefo
@@ -483,7 +505,12 @@ __global__ void __launch_bounds__(256) cross_entropy_bf16_kernel(__nv_bfloat16* 
   __nv_bfloat16* lr = logits + (int64_t)row * ld;
   const int64_t t = targets[row];
   if (t < 0 || t >= V) {
-    if (threadIdx.x == 0) atomicExch(bad_target, 1);
+    if (threadIdx.x == 0) {
+      atomicOr(bad_target, 2);
+      loss_rows[row] = 0.f;
+    }
+    for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8)
+      *reinterpret_cast<uint4*>(lr + c) = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
   if (threadIdx.x == 0) zt_s = __bfloat162float(lr[t]);
@@ -557,7 +584,11 @@ __global__ void __launch_bounds__(256) cross_entropy_warp_kernel(__nv_bfloat16* 
   __nv_bfloat16* lr = logits + (int64_t)row * ld;
   const int64_t t = targets[row];
   if (t < 0 || t >= V) {
-    if (lane == 0) atomicExch(bad_target, 1);
+    if (lane == 0) {
+      atomicOr(bad_target, 2);
+      loss_rows[row] = 0.f;
+    }
+    for (int vi = lane; vi < (V >> 3); vi += 32) reinterpret_cast<uint4*>(lr)[vi] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
   const float zt = __bfloat162float(lr[t]);

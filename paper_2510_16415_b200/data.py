@@ -11,6 +11,8 @@ shipped: pass `corpus_path` (or `text`) for the corpus source.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .errors import ConfigError
@@ -18,6 +20,27 @@ from .pcg import Pcg64Generator
 
 SOURCE_CORPUS = "corpus"
 SOURCE_TEACHER = "teacher"
+
+
+def load_corpus(path: str | None = None) -> str:
+    """data.py:20-24. The reference reads its embedded asset
+    (faultsim/assets/corpus.txt); this package does not ship a copy, so a
+    missing path resolves, in order, to $MECEFO_CORPUS or the asset of an
+    installed `faultsim` package, else raises ConfigError (exit code 2)."""
+    if path is None:
+        path = os.environ.get("MECEFO_CORPUS")
+    if path is None:
+        try:
+            from importlib import resources
+
+            return resources.files("faultsim").joinpath("assets/corpus.txt").read_text("utf-8")
+        except Exception:
+            raise ConfigError("data.source 'corpus' needs data.path (or $MECEFO_CORPUS): the reference's embedded "
+                              "corpus asset is not shipped with this package") from None
+    if not os.path.exists(path):
+        raise ConfigError(f"dataset path does not exist: {path}")
+    with open(path, "r", encoding="utf-8") as f:
+        return f.read()
 
 
 def build_char_vocab(text: str, vocab_size: int) -> dict:
@@ -70,10 +93,7 @@ class ShardedSampler:
         self.n_ranks = n_ranks
         if source == SOURCE_CORPUS:
             if text is None:
-                if corpus_path is None:
-                    raise ConfigError("corpus source needs corpus_path (the reference's embedded asset is not shipped)")
-                with open(corpus_path, "r", encoding="utf-8") as f:
-                    text = f.read()
+                text = load_corpus(corpus_path)
             self.vocab = build_char_vocab(text, vocab_size)
             tokens = encode(text, self.vocab)
             per = len(tokens) // n_ranks

@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib, approx, model as mdl, optim as op, runtime
+from .errors import ContractViolation, NumericalFailure
 from .linalg import SvdConfig
 
 
@@ -101,6 +102,14 @@ class StepEngine:
         self._keep = []
         self.losses = None
         self.graphs = []
+        # device status word (bad token / bad target / non-finite gradient):
+        # kernels set bits, a copy lands in pinned host memory after every
+        # optimizer launch, the host checks it at the next iteration boundary
+        sp = ctypes.c_void_p()
+        _lib.call("mecefo_status_device", self.eng.handle, ctypes.byref(sp))
+        self._status_dev = sp.value
+        _lib.call("mecefo_status_reset", self.eng.handle, runtime.stream_ptr())
+        self._status_host = torch.zeros(4, dtype=torch.int32).pin_memory()
 
     # ------------------------------------------------------------------ utils
     def _gp(self, name: str) -> int:
@@ -113,6 +122,39 @@ class StepEngine:
                                    self._gp(p + "norm_ffn"), alpha_ffn)
         return _lib.LayerGrads(self._gp(p + "q"), self._gp(p + "o"), self._gp(p + "norm_mha"), alpha_mha,
                                self._gp(p + "gate"), self._gp(p + "down"), self._gp(p + "norm_ffn"), alpha_ffn)
+
+    def _memset0(self, t: torch.Tensor) -> None:
+        _lib.call("mecefo_memset_zero", t.data_ptr(), t.numel() * t.element_size(), runtime.stream_ptr())
+
+    def _status_copy(self, stream_ptr: int) -> None:
+        _lib.call("mecefo_status_snapshot", self.eng.handle, self._status_host.data_ptr(), stream_ptr)
+
+    def check_status(self, sync: bool = False) -> None:
+        """Raise what the reference raises for the iteration whose status word
+        reached the host: non-finite gradient -> NumericalFailure
+        (optim.py:55-57); token / target outside the vocabulary ->
+        ContractViolation (model.py:463, 505 raise IndexError there). Without
+        `sync` this reads the latest snapshot (one or two iterations behind);
+        with it, the current one."""
+        if sync:
+            torch.cuda.synchronize()
+        w = int(self._status_host[0])
+        if not w:
+            return
+        _lib.call("mecefo_status_reset", self.eng.handle, runtime.stream_ptr())
+        torch.cuda.synchronize()
+        self._status_host.zero_()
+        if w & _lib.STATUS_NONFINITE_GRAD:
+            raise NumericalFailure("non-finite gradient")
+        what = "token" if w & _lib.STATUS_BAD_TOKEN else "target"
+        raise ContractViolation(f"{what} id outside [0, {self.cfg.vocab})")
+
+    @staticmethod
+    def _check_host_ids(t: torch.Tensor, vocab: int, what: str) -> None:
+        if not t.is_cuda and t.numel():
+            lo, hi = int(t.min()), int(t.max())
+            if lo < 0 or hi >= vocab:
+                raise ContractViolation(f"{what} id outside [0, {vocab}): range [{lo}, {hi}]")
 
     def _dy_buffer(self, k: int) -> torch.Tensor:
         """Compute-precision gradient of layer k's input (k = L: the head's
@@ -204,6 +246,8 @@ class StepEngine:
         w = self.weights
         ws, wn = self.ws.data_ptr(), self.ws.numel()
         for i, m_ in enumerate(mbs):
+            self._check_host_ids(m_.tokens, cfg.vocab, "token")
+            self._check_host_ids(m_.targets, cfg.vocab, "target")
             self.tok[i * b1:(i + 1) * b1].copy_(m_.tokens.reshape(-1), non_blocking=True)
             self.tgt[i * b1:(i + 1) * b1].copy_(m_.targets.reshape(-1), non_blocking=True)
         _lib.call("mecefo_embedding_forward", eng.handle, self.tok.data_ptr(),
@@ -286,21 +330,22 @@ class StepEngine:
         host, dev, ev = self._seg_slot(slot, 0)
         if fill:
             ev.synchronize()  # the copy that last read this slot has executed
-            arr, max_numel, names = op.adam_segments(self.weights, self.opt, lr, skip)
+            arr, total_numel, names = op.adam_segments(self.weights, self.opt, lr, skip)
             host.numpy()[: arr.nbytes] = arr.view(np.uint8)
             for name in names:
                 self.opt.step[name] = self.opt.step.get(name, 0) + 1
-            self._adam_meta = (len(names), max_numel)
-        nseg, max_numel = self._adam_meta
+            self._adam_meta = (len(names), total_numel)
+        nseg, total_numel = self._adam_meta
         dev.copy_(host, non_blocking=True)
         if record:
             ev.record()
         if nseg:
             cfg = self.opt.cfg
             shadow = self.weights.shadow.data_ptr() if self.precision != "fp32" else None
-            _lib.call("mecefo_adamw_step", self.eng.handle, dev.data_ptr(), nseg, max_numel,
+            _lib.call("mecefo_adamw_step", self.eng.handle, dev.data_ptr(), nseg, total_numel,
                       self.weights.master.data_ptr(), self.grad.data_ptr(), self.opt.m.data_ptr(),
                       self.opt.v.data_ptr(), shadow, cfg.beta1, cfg.beta2, cfg.eps, stream_ptr)
+        self._status_copy(stream_ptr)
 
     # ---------------------------------------------------------------- step
     def _prerefresh(self, mbs: list) -> None:
@@ -345,8 +390,8 @@ class StepEngine:
 
     def _body(self, mbs: list, losses: torch.Tensor) -> None:
         self._prerefresh(mbs)
-        self.grad.zero_()
-        losses.zero_()
+        self._memset0(self.grad)
+        self._memset0(losses)
         if self._fusable(mbs):
             ranks = [mb.rank for mb in mbs]
             if ranks == list(range(ranks[0], ranks[0] + len(ranks))):
@@ -368,11 +413,14 @@ class StepEngine:
     def step(self, mbs: list, n_ranks: int, lr: float, skip=(), check: bool = True) -> torch.Tensor:
         """Run this GPU's microbatches, exchange, update (eager launches).
         Returns the (n_ranks,) device vector of per-rank losses."""
+        self.check_status()
         if self.losses is None or self.losses.numel() != n_ranks:
             self.losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
         self._body(mbs, self.losses)
         if check:
             op.apply_flat(self.weights, self.opt, self.grad, lr, skip=skip, check=True)
+            self._status_copy(runtime.stream_ptr())
+            self.check_status(sync=True)
         else:
             self.opt.ensure_flat(self.weights.total, self.device)
             slot = self._seg_k = (getattr(self, "_seg_k", 0) + 1) % 2
@@ -387,8 +435,8 @@ class StepEngine:
         if self.losses is None or self.losses.numel() != n_ranks:
             self.losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
         self._seg_slot(0, 0)
-        arr, max_numel, names = op.adam_segments(self.weights, self.opt, 1e-4, skip)
-        self._adam_meta = (len(names), max_numel)
+        arr, total_numel, names = op.adam_segments(self.weights, self.opt, 1e-4, skip)
+        self._adam_meta = (len(names), total_numel)
         self._graph_plan = (list(mbs), n_ranks, tuple(skip))
         torch.cuda.synchronize()
         steps = {k: pc.step for k, pc in self.projs.items()}
@@ -407,6 +455,7 @@ class StepEngine:
     def replay(self, lr: float) -> torch.Tensor:
         """One captured iteration: host bookkeeping (optimizer scalars,
         projection step counters) then a single graph launch."""
+        self.check_status()
         mbs, n_ranks, skip = self._graph_plan
         slot = self._seg_k = (getattr(self, "_seg_k", 0) + 1) % 2
         host, dev, ev = self._segs[slot]

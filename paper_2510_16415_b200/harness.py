@@ -60,7 +60,9 @@ class CostSettings:
 
 @dataclass
 class DataSettings:
-    source: str = "synthetic"
+    """harness.py:54-56: the reference default is the embedded char corpus.
+    "synthetic" (uniform tokens) is this engine's explicit opt-in."""
+    source: str = "corpus"
     path: str | None = None
 
 
@@ -79,6 +81,8 @@ class RunConfig:
             raise ConfigError("cluster layer count must match the model")
         if self.run.global_batch % self.cluster.dp != 0:
             raise ConfigError("global batch must divide evenly across DP ranks")
+        if self.data.path is not None and not os.path.exists(self.data.path):  # harness.py:74-75
+            raise ConfigError(f"dataset path does not exist: {self.data.path}")
 
     @property
     def per_rank_batch(self) -> int:

@@ -75,12 +75,13 @@ def lr_at(step: int, total_steps: int, base_lr: float, floor_fraction: float = 0
 
 def adam_segments(weights, state: OptimState, lr_t: float, skip=()) -> tuple[np.ndarray, int, list]:
     """Host side of apply_step: per-parameter bias corrections for the
-    parameters that step this iteration (advancing their counters)."""
+    parameters that step this iteration. Returns (segments, total numel,
+    names); the caller advances the counters of `names`."""
     cfg = state.cfg
     skip = set(skip)
     segs = []
     names = []
-    max_numel = 0
+    total_numel = 0
     for name, shape, off in weights.layout:
         if name in skip:
             continue
@@ -88,12 +89,12 @@ def adam_segments(weights, state: OptimState, lr_t: float, skip=()) -> tuple[np.
         n = int(np.prod(shape))
         segs.append((off, n, lr_t / (1.0 - cfg.beta1 ** t), 1.0 / (1.0 - cfg.beta2 ** t), lr_t * cfg.weight_decay))
         names.append(name)
-        max_numel = max(max_numel, n)
+        total_numel += n
     arr = np.zeros(len(segs), dtype=[("offset", "<i8"), ("numel", "<i8"), ("step_size", "<f4"), ("inv_bc2", "<f4"),
                                      ("lr_wd", "<f4"), ("pad", "<i4")])
     for k, s in enumerate(segs):
         arr[k] = (*s, 0)
-    return arr, max_numel, names
+    return arr, total_numel, names
 
 
 def apply_flat(weights, state: OptimState, flat_grad: torch.Tensor, lr_t: float, skip=(), check: bool = True,
@@ -123,13 +124,13 @@ def apply_flat(weights, state: OptimState, flat_grad: torch.Tensor, lr_t: float,
             state.step[name] = state.step.get(name, 0) + 1
         weights.sync_shadow()
         return
-    arr, max_numel, names = adam_segments(weights, state, lr_t, skip)
+    arr, total_numel, names = adam_segments(weights, state, lr_t, skip)
     if len(names) == 0:
         return
     segs = torch.from_numpy(arr.view(np.uint8)).to(weights.master.device, non_blocking=True)
     eng = runtime.engine_for(weights.cfg, weights.precision)
     shadow = weights.shadow.data_ptr() if weights.precision != "fp32" else None
-    _lib.call("mecefo_adamw_step", eng.handle, segs.data_ptr(), len(names), max_numel, weights.master.data_ptr(),
+    _lib.call("mecefo_adamw_step", eng.handle, segs.data_ptr(), len(names), total_numel, weights.master.data_ptr(),
               flat_grad.data_ptr(), state.m.data_ptr(), state.v.data_ptr(), shadow, cfg.beta1, cfg.beta2, cfg.eps, sp)
     for name in names:
         state.step[name] = state.step.get(name, 0) + 1

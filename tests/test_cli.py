@@ -70,3 +70,21 @@ def test_unrecoverable_cluster_exit_4(tmp_path, capsys):
     cfg["scenario"] = {"kind": "per_iteration", "probability": 1.0, "recovery_iterations": 1000000000}
     assert cli.main(["train", "--config", _write(tmp_path, cfg), "--quiet"]) == cli.EXIT_UNRECOVERABLE
     assert "unrecoverable" in capsys.readouterr().err
+
+
+def test_data_defaults_follow_reference(tmp_path, monkeypatch):
+    """harness.py:54-56: the default source is the corpus; harness.py:74-75:
+    a configured data.path must exist (ConfigError -> exit 2)."""
+    assert harness.DataSettings().source == "corpus"
+    bad = json.loads(json.dumps(C0))
+    bad["data"] = {"source": "corpus", "path": str(tmp_path / "nope.txt")}
+    with pytest.raises(harness.ConfigError):
+        harness.config_from_dict(bad)
+    assert cli.main(["train", "--config", _write(tmp_path, bad), "--quiet"]) == cli.EXIT_CONFIG
+    # corpus without a path and no asset available: explicit ConfigError, not a traceback
+    from paper_2510_16415_b200 import data
+
+    monkeypatch.delenv("MECEFO_CORPUS", raising=False)
+    monkeypatch.setattr("importlib.resources.files", lambda pkg: (_ for _ in ()).throw(ModuleNotFoundError(pkg)))
+    with pytest.raises(harness.ConfigError, match="data.path"):
+        data.load_corpus(None)

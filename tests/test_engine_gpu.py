@@ -79,33 +79,45 @@ def test_eq1_weighted_gradients_match_reference_aggregation(cuda, prec, tol, R_,
 
 @pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("bf16", 5e-2)])
 def test_step_with_adamw_matches_reference(cuda, prec, tol):
+    """Three MeCeFO steps. Each step's Eq. (1) gradients are checked against
+    the oracle (gradient tolerance), then the oracle's AdamW (optim.py:75-103)
+    applies the ENGINE's gradient to the float64 weights, so the weight
+    comparison isolates the fused optimizer: <= 1% of elements may differ by
+    more than 1e-3 of the update scale (fp32 vs fp64 arithmetic)."""
+    from paper_2510_16415_b200 import optim as op
+
     batches = _batches(2, 2, seed=3)
     eng, bases = _engine(prec, 2)
     mbs, lean, skip = _plan(2, {1}, batches)
     W = R.init_params(D0, 0)
     opt = optim_ref.Adam()
+    losses = torch.zeros(2, device="cuda")
     for it in range(3):
         lr = optim_ref.lr_at(it + 1, 3, 1e-3)
-        eng.step(mbs, 2, lr, skip=skip, check=True)
+        eng._body(mbs, losses)
+        torch.cuda.synchronize()
+        got = {name: eng.grad[off: off + int(np.prod(shape))].view(shape).double().cpu().numpy()
+               for name, shape, off in eng.weights.layout}
+        op.apply_flat(eng.weights, eng.opt, eng.grad, lr, skip=skip, check=True)
         per_rank = [R.rank_pass(D0, W, batches[j][0], batches[j][1], ["ffn_input_only"] * 2,
                                 {l: bases[(j, l)] for l in range(2)})[1] for j in range(2)]
         active = {(l, k): ([] if k in cluster_ref.MHA else [0, 1]) for l in range(2)
                   for k in cluster_ref.MHA + cluster_ref.FFN}
         avg, skipped = cluster_ref.aggregate(per_rank, active, 2)
-        opt.apply(W, avg, lr, skip=skipped)
-    # Adam normalises each element's update to ~lr, so an element whose tiny
-    # gradient flips sign under fp32 rounding moves by ~2 lr: bound the weight
-    # error by the update scale, and require almost all elements to agree.
+        for name in avg:
+            assert R.rel_err(got[name], avg[name]) < tol, (it, name)
+        opt.apply(W, {n: got[n] for n in avg}, lr, skip=skipped)
+    torch.cuda.synchronize()
     W0 = R.init_params(D0, 0)
     for name, t in eng.weights.named():
         if name in skipped:
             continue  # checked exactly below
-        got = t.cpu().numpy().astype(np.float64)
-        err = np.abs(got - W[name])
+        w = t.cpu().numpy().astype(np.float64)
+        err = np.abs(w - W[name])
         step = np.abs(W[name] - W0[name]).max() + 1e-6 * np.abs(W0[name]).max()  # + fp32 rounding of w
-        assert err.max() <= 2.5 * step, name
-        frac_bad = float((err > (1e-4 if prec == "fp32" else 3e-2) * step).mean())
-        assert frac_bad < (1e-2 if prec == "fp32" else 1e-1), (name, frac_bad)
+        assert err.max() <= 0.05 * step, name
+        frac_bad = float((err > 1e-3 * step).mean())
+        assert frac_bad <= 1e-2, (name, frac_bad)
     # skipped MHA params never moved, and their step counters never advanced
     assert np.array_equal(eng.weights.get("layers.0.q").cpu().numpy(),
                           R.init_params(D0, 0)["layers.0.q"].astype(np.float32))
