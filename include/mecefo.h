@@ -322,6 +322,36 @@ size_t mecefo_subspace_workspace_bytes(const mecefo_subspace_job* jobs, int32_t 
 int mecefo_subspace_iteration_batched(mecefo_engine* e, const mecefo_subspace_job* jobs, int32_t count,
                                       int32_t iterations, void* workspace, size_t workspace_bytes, void* stream);
 
+/* One matrix of a CONVERGED projection refresh (linalg.py:97-142): the
+ * orthonormal top-r right singular basis of W, returned once every kept Ritz
+ * pair satisfies ||W^T W v - theta v|| <= tol * theta_max (linalg.py:131-135),
+ * in float64. Host array of jobs; device pointers inside. */
+typedef struct mecefo_refresh_job {
+  const float* w;     /* rows x cols fp32, row stride ldw */
+  int64_t rows, cols, ldw;
+  int32_t r;          /* basis rank, 1 <= r <= cols (approx.py:79: min(r, in)) */
+  int32_t k;          /* block width r + oversample, r <= k <= min(cols, 1024) */
+  const double* v0;   /* cols x k (ld k) orthonormal start block: QR of the
+                         seeded Gaussian (linalg.py:117) */
+  float* v1;          /* out: cols x r (ld r) basis, fp32 */
+  double* v1_f64;     /* optional out: the same in fp64 */
+  double* theta;      /* optional out: the r Ritz values (sigma^2), descending */
+  double residual;    /* out (host): final relative residual */
+  int32_t products;   /* out (host): block products with W^T W (or W W^T) spent */
+  int32_t converged;  /* out (host): 1 if residual <= tol */
+} mecefo_refresh_job;
+
+/* Chebyshev-filtered block subspace iteration with Rayleigh-Ritz, all
+ * matrices of a refresh batched per phase (fp64 DMMA GEMMs, CholeskyQR2,
+ * Jacobi Ritz solve), wide matrices iterated on W W^T and checked on W^T W.
+ * At most max_products block products per matrix (the reference's
+ * max_iterations budget, one product per iteration there). Synchronises the
+ * stream once per outer iteration. MECEFO_ERR_SVD_NOCONV (SvdConvergenceError)
+ * if any job misses tol; each job's residual/products are filled in either way. */
+size_t mecefo_refresh_workspace_bytes(const mecefo_refresh_job* jobs, int32_t count);
+int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t count, double tol,
+                             int32_t max_products, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernels this library has launched (evidence counter). */
 int64_t mecefo_launch_count(void);
 

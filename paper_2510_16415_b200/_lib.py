@@ -123,6 +123,24 @@ class SubspaceJob(ctypes.Structure):
     ]
 
 
+class RefreshJob(ctypes.Structure):
+    _fields_ = [
+        ("w", c_void_p),
+        ("rows", c_int64),
+        ("cols", c_int64),
+        ("ldw", c_int64),
+        ("r", c_int32),
+        ("k", c_int32),
+        ("v0", c_void_p),
+        ("v1", c_void_p),
+        ("v1_f64", c_void_p),
+        ("theta", c_void_p),
+        ("residual", ctypes.c_double),
+        ("products", c_int32),
+        ("converged", c_int32),
+    ]
+
+
 class FfnSaved(ctypes.Structure):
     _fields_ = [("h2", c_void_p), ("act", c_void_p), ("dcat", c_void_p)]
 
@@ -225,6 +243,10 @@ _SIGNATURES = {
     "mecefo_lowrank_batched_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32, c_int32]),
     "mecefo_lowrank_wgrads_batched": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_size_t, c_void_p]),
     "mecefo_subspace_workspace_bytes": (c_size_t, [c_void_p, c_int32]),
+    "mecefo_refresh_workspace_bytes": (c_size_t, [c_void_p, c_int32]),
+    "mecefo_refresh_converged": (
+        c_int, [c_void_p, c_void_p, c_int32, ctypes.c_double, c_int32, c_void_p, c_size_t, c_void_p],
+    ),
     "mecefo_subspace_iteration_batched": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_size_t, c_void_p]),
 }
 

@@ -16,7 +16,7 @@ import torch
 
 from . import _lib, model as mdl, runtime
 from .errors import ContractViolation
-from .linalg import SvdConfig, top_r_right_singular_vectors
+from .linalg import SvdConfig, refresh_bases, top_r_right_singular_vectors
 
 FFN_KINDS = mdl.FFN_WEIGHT_KINDS
 
@@ -145,11 +145,18 @@ def refresh_projections(cache: ProjectionCache, lw: mdl.LayerWeights, svd: SvdCo
     if cache.basis and getattr(cache, "_fresh_step", None) == cache.step:
         return  # already refreshed for this step by a batched pre-refresh
     cache.refreshes += 1
-    for kind in FFN_KINDS:
-        w = lw.kind(kind)
-        rank = min(cache.rank, w.shape[1])
-        cfg = SvdConfig(rank=rank, tolerance=svd.tolerance, max_iterations=svd.max_iterations, seed=svd.seed)
-        cache.set_basis(kind, top_r_right_singular_vectors(w, cfg, budgeted=budgeted))
+    mats = [lw.kind(kind) for kind in FFN_KINDS]
+    ranks = [min(cache.rank, w.shape[1]) for w in mats]
+    if budgeted:
+        for kind, w, rank in zip(FFN_KINDS, mats, ranks):
+            cfg = SvdConfig(rank=rank, tolerance=svd.tolerance, max_iterations=svd.max_iterations, seed=svd.seed)
+            cache.set_basis(kind, top_r_right_singular_vectors(w, cfg, budgeted=True))
+            cache.svd_calls += 1
+        return
+    # the three kinds in one batched device solve (each is linalg.py:97-142
+    # with SvdConfig(rank=min(r, in), svd.tolerance, svd.max_iterations, svd.seed))
+    for kind, v1 in zip(FFN_KINDS, refresh_bases(mats, ranks, svd)):
+        cache.set_basis(kind, v1)
         cache.svd_calls += 1
 
 

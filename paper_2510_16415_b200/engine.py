@@ -61,8 +61,10 @@ class StepEngine:
         self.tau = tau
         self.svd = svd if svd is not None else SvdConfig(rank=r, tolerance=1e-9, max_iterations=3000, seed=seed + 23)
         self.svd_budgeted = svd_budgeted
-        # budgeted runs refresh all due bases in one batched device iteration
-        self.batched_refresh = svd_budgeted
+        # every due basis of an iteration is refreshed in ONE batched device
+        # solve (converged to svd.tolerance, or the budgeted fixed iteration)
+        self.batched_refresh = True
+        self.refresh_info: list = []
         self.group = group
         self.opt = op.OptimState(optim_cfg or op.OptimConfig())
         self.opt.ensure_flat(self.weights.total, self.device)
@@ -367,8 +369,6 @@ class StepEngine:
                 due.setdefault(l, []).append(pc)
         if not due:
             return
-        from .linalg import top_r_right_singular_vectors_batched
-
         mats, ranks, owners = [], [], []
         for l, pcs in due.items():
             for kind in approx.FFN_KINDS:
@@ -376,7 +376,7 @@ class StepEngine:
                 mats.append(w)
                 ranks.append(min(self.r, w.shape[1]))
                 owners.append((l, kind))
-        bases = top_r_right_singular_vectors_batched(mats, ranks, self.svd.max_iterations, self.svd.seed)
+        bases = self._solve_bases(mats, ranks)
         for (l, kind), v1 in zip(owners, bases):
             for pc in due[l]:
                 pc.set_basis(kind, v1)
@@ -387,6 +387,16 @@ class StepEngine:
                 pc.refreshes += 1
                 pc.svd_calls += len(approx.FFN_KINDS)
                 pc._fresh_step = pc.step
+
+    def _solve_bases(self, mats: list, ranks: list) -> list:
+        from .linalg import refresh_bases, top_r_right_singular_vectors_batched
+
+        if self.svd_budgeted:
+            return top_r_right_singular_vectors_batched(mats, ranks, self.svd.max_iterations, self.svd.seed)
+        info = []
+        out = refresh_bases(mats, ranks, self.svd, info=info)
+        self.refresh_info = info
+        return out
 
     def _body(self, mbs: list, losses: torch.Tensor) -> None:
         self._prerefresh(mbs)
@@ -507,9 +517,7 @@ class StepEngine:
                         pc = approx.ProjectionCache(rank=self.r, refresh_period=self.tau)
                         approx.refresh_projections(pc, self.weights.layers[l], self.svd, budgeted=self.svd_budgeted)
         if mats:
-            from .linalg import top_r_right_singular_vectors_batched
-
-            top_r_right_singular_vectors_batched(mats, ranks, self.svd.max_iterations, self.svd.seed)
+            self._solve_bases(mats, ranks)
         torch.cuda.synchronize()
         return time.perf_counter() - t0
 

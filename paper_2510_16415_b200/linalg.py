@@ -2,13 +2,16 @@
 
 * seeded_gaussian: host PCG64 draws, bit-identical to the reference (used for
   weight init and the subspace-iteration start block).
-* top_r_right_singular_vectors: the reference's block power iteration on
-  W^T W (oversample 4, QR, Rayleigh-Ritz, relative-residual stop). The two
-  large products per iteration (W^T W once, then B V) run on the engine's
-  fp32 GEMM; the k x k factorizations (k = r + 4) run in host float64, as in
-  the reference. This is the tau-amortised projection refresh
-  (approx.py:66-87), not part of the per-step hot path; SURVEY.md §8(f) row 3
-  lists a fully on-device refresh as the next step.
+* top_r_right_singular_vectors / refresh_bases: the top-r right singular
+  subspace of W to the reference's stopping rule (residual <= tol * theta_max,
+  SvdConvergenceError otherwise; linalg.py:97-142), computed entirely on the
+  device in float64 (mecefo_refresh_converged: Chebyshev-filtered block
+  subspace iteration + Rayleigh-Ritz, all due matrices of a refresh batched;
+  csrc/refresh.cu). This is the tau-amortised projection refresh
+  (approx.py:66-87).
+* top_r_right_singular_vectors_batched: the budgeted fixed-iteration variant
+  (30 iterations, the cost model's charge, costmodel.py:41) kept for
+  throughput comparisons; it does NOT meet the stopping rule.
 """
 
 from __future__ import annotations
@@ -23,10 +26,15 @@ from .errors import ContractViolation, SvdConvergenceError
 
 __all__ = ["SvdConfig", "check_matrix", "seeded_gaussian", "top_r_right_singular_vectors"]
 
-# fp32 device products bound the attainable relative residual; tolerances
-# tighter than this are clamped (the reference runs in float64).
-FP32_RESIDUAL_FLOOR = 2e-6
-_OVERSAMPLE = 4  # linalg.py:94
+_OVERSAMPLE = 4  # linalg.py:94 (the minimum; see oversample_for)
+
+
+def oversample_for(r: int) -> int:
+    """Extra block columns of the converged refresh: the reference carries 4
+    (linalg.py:94); a wider block widens the gap the filter separates
+    (lambda_r vs lambda_k) and cuts the iteration count. Only span(V[:, :r])
+    is returned, so the computed object is unchanged."""
+    return max(_OVERSAMPLE, min(r // 4, 32))
 
 
 def seeded_gaussian(rows: int, cols: int, mean: float = 0.0, stddev: float = 1.0, seed: int = 0) -> np.ndarray:
@@ -78,56 +86,82 @@ def _fp32_engine():
     return eng
 
 
+_START64: dict = {}
+
+
+def _start_block64(n: int, k: int, seed: int, device) -> torch.Tensor:
+    """QR of the seeded Gaussian start block (linalg.py:117), float64, cached
+    per (n, k, seed) — every refresh with the same SvdConfig starts there."""
+    key = (n, k, seed, str(device))
+    if key not in _START64:
+        v, _ = np.linalg.qr(seeded_gaussian(n, k, 0.0, 1.0, seed))
+        _START64[key] = torch.from_numpy(np.ascontiguousarray(v)).to(device)
+    return _START64[key]
+
+
+def refresh_bases(ws: list, ranks: list, svd: SvdConfig, oversample: int | None = None, info: list | None = None,
+                  want_f64: bool = False):
+    """Converged top-r right singular bases of several matrices at once
+    (linalg.py:97-142 per matrix, batched like approx.py:66-87 refreshes
+    every kind). Returns fp32 (cols, r) CUDA tensors (and fp64 copies with
+    want_f64). Raises SvdConvergenceError(residual) if any matrix misses
+    svd.tolerance within svd.max_iterations block products. `info`, if
+    given, receives one dict per matrix (residual, products, k)."""
+    from . import _lib
+
+    if not ws:
+        return []
+    dev = torch.device("cuda", torch.cuda.current_device())
+    jobs = (_lib.RefreshJob * len(ws))()
+    keep, outs, outs64 = [], [], []
+    for i, (w, r) in enumerate(zip(ws, ranks)):
+        if w.ndim != 2:
+            raise ContractViolation(f"w must be 2-D, got shape {tuple(w.shape)}")
+        wd = torch.as_tensor(w).detach()
+        if wd.device != dev or wd.dtype != torch.float32 or wd.stride(1) != 1:
+            wd = wd.to(device=dev, dtype=torch.float32).contiguous()
+        rows, n = wd.shape
+        if not 1 <= r <= n:
+            raise ContractViolation(f"rank {r} exceeds the column count of {tuple(wd.shape)}")
+        k = min(n, r + (oversample if oversample is not None else oversample_for(r)))
+        v0 = _start_block64(n, k, svd.seed, dev)
+        v1 = torch.empty(n, r, dtype=torch.float32, device=dev)
+        v64 = torch.empty(n, r, dtype=torch.float64, device=dev) if want_f64 else None
+        jobs[i] = _lib.RefreshJob(wd.data_ptr(), rows, n, wd.stride(0), r, k, v0.data_ptr(), v1.data_ptr(),
+                                  v64.data_ptr() if v64 is not None else None, None, 0.0, 0, 0)
+        keep += [wd, v0]
+        outs.append(v1)
+        outs64.append(v64)
+    lib = _lib.load()
+    nbytes = int(lib.mecefo_refresh_workspace_bytes(jobs, len(ws)))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    rc = lib.mecefo_refresh_converged(None, jobs, len(ws), float(svd.tolerance), int(svd.max_iterations),
+                                      scratch.data_ptr(), nbytes, runtime.stream_ptr())
+    if info is not None:
+        info.extend({"residual": jobs[i].residual, "products": jobs[i].products,
+                     "k": jobs[i].k, "converged": bool(jobs[i].converged)} for i in range(len(ws)))
+    if rc == 3:
+        worst = max(jobs[i].residual for i in range(len(ws)) if not jobs[i].converged)
+        raise SvdConvergenceError(
+            f"subspace iteration did not converge within {svd.max_iterations} iterations "
+            f"(last residual {worst:.3e})", residual=worst)
+    _lib.check(rc)
+    del keep, scratch
+    return (outs, outs64) if want_f64 else outs
+
+
 def top_r_right_singular_vectors(w: torch.Tensor, cfg: SvdConfig, budgeted: bool = False) -> torch.Tensor:
     """Orthonormal (cols x r) basis of the top-r right singular subspace of w
-    (linalg.py:97-142). Returns a float32 CUDA tensor.
-
-    budgeted=True stops after cfg.max_iterations without raising (used for
-    throughput runs, where the basis quality does not affect timing)."""
+    (linalg.py:97-142), float32 CUDA tensor. Converged to cfg.tolerance on the
+    device (refresh_bases); budgeted=True instead runs exactly
+    cfg.max_iterations iterations of the budgeted batched iteration without a
+    stopping rule (throughput comparisons only)."""
     if w.ndim != 2:
         raise ContractViolation(f"w must be 2-D, got shape {tuple(w.shape)}")
     cfg.validate_for(w.shape)
-    n = w.shape[1]
-    r = cfg.rank
-    eng = _fp32_engine()
-    wd = w.detach().to(device="cuda", dtype=torch.float32).contiguous()
-    check_matrix(wd, "w")
-    B = torch.empty(n, n, dtype=torch.float32, device=wd.device)
-    # B = W^T W: A(i, k) = W[k, i] and B(j, k) = W[k, j], both MN-major.
-    runtime.gemm(eng, wd, False, wd, False, n, n, wd.shape[0], B)
-    scale = float(torch.linalg.matrix_norm(B.double()).item())
-    if scale == 0.0:
-        return torch.eye(n, device=wd.device)[:, :r].contiguous()
-    k = min(n, r + _OVERSAMPLE)
-    tol = max(cfg.tolerance, FP32_RESIDUAL_FLOOR)
-    V, _ = np.linalg.qr(seeded_gaussian(n, k, 0.0, 1.0, cfg.seed))
-    Vd = torch.empty(n, k, dtype=torch.float32, device=wd.device)
-    Zd = torch.empty(n, k, dtype=torch.float32, device=wd.device)
-    last = np.inf
-    for _ in range(cfg.max_iterations):
-        Vd.copy_(torch.from_numpy(np.ascontiguousarray(V, dtype=np.float32)))
-        # Z = B V: A = B (K-major, symmetric), B-operand(n=j, k) = V[k, j] MN-major
-        runtime.gemm(eng, B, True, Vd, False, n, k, n, Zd)
-        V, _ = np.linalg.qr(Zd.double().cpu().numpy())
-        Vd.copy_(torch.from_numpy(np.ascontiguousarray(V, dtype=np.float32)))
-        runtime.gemm(eng, B, True, Vd, False, n, k, n, Zd)
-        BV = Zd.double().cpu().numpy()
-        small = V.T @ BV
-        theta, s = np.linalg.eigh(0.5 * (small + small.T))
-        order = np.argsort(theta)[::-1]
-        theta = theta[order]
-        V = V @ s[:, order]
-        top = V[:, :r]
-        resid = BV @ s[:, order][:, :r] - top * theta[:r]
-        last = float(np.max(np.linalg.norm(resid, axis=0)) / max(theta[0], np.finfo(float).tiny))
-        if last <= tol:
-            return torch.from_numpy(np.ascontiguousarray(top)).to(wd.device, torch.float32)
     if budgeted:
-        return torch.from_numpy(np.ascontiguousarray(V[:, :r])).to(wd.device, torch.float32)
-    raise SvdConvergenceError(
-        f"subspace iteration did not converge within {cfg.max_iterations} iterations (last residual {last:.3e})",
-        residual=last,
-    )
+        return top_r_right_singular_vectors_batched([w], [cfg.rank], cfg.max_iterations, cfg.seed)[0]
+    return refresh_bases([w], [cfg.rank], cfg)[0]
 
 
 _START_CACHE: dict = {}
