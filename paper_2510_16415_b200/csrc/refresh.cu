@@ -171,7 +171,7 @@ size_t mecefo_refresh_workspace_bytes(const mecefo_refresh_job* jobs, int32_t co
     total = al256(total + p.bytes);
     kmax = std::max(kmax, jobs[i].k);
   }
-  const size_t slot = al256((size_t)count * std::max(sizeof(DJob), std::max(sizeof(SmallJob), sizeof(ResJob) + sizeof(CopyJob) + sizeof(AxJob))));
+  const size_t slot = al256(2 * (size_t)count * std::max(sizeof(DJob), std::max(sizeof(SmallJob), sizeof(ResJob) + sizeof(CopyJob) + sizeof(AxJob))));
   total += kSlots * slot;
   total += al256((size_t)count * (kmax + 1) * sizeof(double));
   return total + 1024;
@@ -188,6 +188,7 @@ int run_small(Ctx& cx, const void* kern, std::vector<SmallJob>& js, size_t smem)
   TRY(rc);
   CUDA_TRY(cudaMemcpyAsync(d, js.data(), js.size() * sizeof(SmallJob), cudaMemcpyHostToDevice, cx.s));
   if (smem > 0) TRY(ensure_smem(kern, (int)smem));
+  ProfScope prof(kern == (const void*)cholqr_kernel ? "refresh.cholqr" : "refresh.jacobi", 0.0, 0.0, cx.s);
   void* args[] = {&d};
   CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)js.size()), dim3(RF_SMALL_THREADS), args, smem, cx.s));
   return check_launch(kern == (const void*)cholqr_kernel ? "cholqr_kernel" : "jacobi_eig_kernel");
@@ -215,7 +216,7 @@ int qr2(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<double*>& Z, std::vector<
       const size_t need = ((size_t)pp->k * (pp->k | 1) + 2 * (size_t)pp->k) * 8;
       const int use = need <= kSmemLimit - 1024 ? 1 : 0;
       if (use) smem = std::max(smem, need);
-      sj.push_back(SmallJob{pp->S, pp->Mk, nullptr, pp->scr, pp->k, use});
+      sj.push_back(SmallJob{pp->S, pp->Mk, nullptr, pp->scr, pp->k, use, 0.0});
     }
     TRY(run_small(cx, (const void*)cholqr_kernel, sj, smem));
     std::vector<DJob> m;
@@ -259,10 +260,13 @@ int rayleigh_ritz(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<int>& idx) {
   size_t smem = 0;
   for (size_t i = 0; i < ps.size(); ++i) {
     RfPlan& p = *ps[i];
-    const size_t need = (size_t)p.k * (p.k | 1) * 8;
-    const int use = need <= kSmemLimit - 8 * 1024 ? 1 : 0;
+    const size_t need = (((size_t)p.k * (p.k + 1) / 2 + 1) / 2 * 2 + (size_t)p.k * p.k) * 8;
+    const int use = need <= kSmemLimit - 14 * 1024 ? 1 : 0;
     if (use) smem = std::max(smem, need);
-    sj.push_back(SmallJob{p.S, p.Uk, cx.summary + (size_t)idx[i] * (cx.kmax + 1), p.scr, p.k, use});
+    // Jacobi accuracy follows the outer residual: early Ritz steps need only
+    // a rough rotation (Frobenius off-mass 1e-8 x the residual, squared)
+    const double rel = std::min(1e-6, std::max(1e-15, 1e-4 * p.resid));
+    sj.push_back(SmallJob{p.S, p.Uk, cx.summary + (size_t)idx[i] * (cx.kmax + 1), p.scr, p.k, use, rel * rel});
   }
   TRY(run_small(cx, (const void*)jacobi_eig_kernel, sj, smem));
   for (auto* pp : ps) {
@@ -289,6 +293,7 @@ int rayleigh_ritz(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<int>& idx) {
   void* d = cx.next_slot(rj.size() * sizeof(ResJob), &rc);
   TRY(rc);
   CUDA_TRY(cudaMemcpyAsync(d, rj.data(), rj.size() * sizeof(ResJob), cudaMemcpyHostToDevice, cx.s));
+  ProfScope prof("refresh.residual", 0.0, 0.0, cx.s);
   residual_kernel<<<(unsigned)rj.size(), 1024, 0, cx.s>>>(reinterpret_cast<const ResJob*>(d));
   return check_launch("residual_kernel");
 }
@@ -305,6 +310,7 @@ int axpby(Ctx& cx, std::vector<AxJob>& js) {
   TRY(rc);
   CUDA_TRY(cudaMemcpyAsync(d, js.data(), js.size() * sizeof(AxJob), cudaMemcpyHostToDevice, cx.s));
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 8 * kNumSMs);
+  ProfScope prof("refresh.axpby", 0.0, 0.0, cx.s);
   axpby_f64_kernel<<<(unsigned)blocks, 256, 0, cx.s>>>(reinterpret_cast<const AxJob*>(d), (int)js.size(), total);
   return check_launch("axpby_f64_kernel");
 }
@@ -364,7 +370,7 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
   }
   Ctx cx;
   cx.s = reinterpret_cast<cudaStream_t>(stream);
-  cx.slot_bytes = al256((size_t)count * std::max(sizeof(DJob), std::max(sizeof(SmallJob), sizeof(ResJob) + sizeof(CopyJob) + sizeof(AxJob))));
+  cx.slot_bytes = al256(2 * (size_t)count * std::max(sizeof(DJob), std::max(sizeof(SmallJob), sizeof(ResJob) + sizeof(CopyJob) + sizeof(AxJob))));
   cx.arena = base + off;
   off += kSlots * cx.slot_bytes;
   cx.summary = reinterpret_cast<double*>(base + off);
@@ -577,7 +583,11 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
       ee[q] = 0.5 * a;
       const double xmax = (1.05 * t0 - cc[q]) / ee[q];
       int d = 1;
-      if (xmax > 1.0 + 1e-12 && p.k < p.n) d = (int)std::floor(std::acosh(1e6) / std::acosh(xmax));
+      // amplification ceiling T_d(x_max): 1e6 while the block is rough, up to
+      // 1e10 as the Ritz vectors converge (their contamination x the ratio
+      // stays far below the columns' own signal)
+      const double lim = std::max(1e6, std::min(1e10, 1e2 / std::max(p.resid, 1e-30)));
+      if (xmax > 1.0 + 1e-12 && p.k < p.n) d = (int)std::floor(std::acosh(lim) / std::acosh(xmax));
       if (p.k >= p.n) d = 1;
       d = std::max(1, std::min(d, 24));
       d = std::min(d, std::max(1, max_products - p.products - 1));

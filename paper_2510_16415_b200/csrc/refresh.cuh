@@ -158,6 +158,7 @@ struct SmallJob {
   double* scratch;  // global fallback for the work matrices
   int k;
   int use_smem;
+  double tol2;      // jacobi: stop when off-diagonal mass <= tol2 * total (Frobenius^2)
 };
 
 __device__ __forceinline__ double blk_sum_d(double v, double* red) {
@@ -246,42 +247,114 @@ __global__ void __launch_bounds__(RF_SMALL_THREADS) cholqr_kernel(const SmallJob
 
 // Rayleigh-Ritz eigensolve (linalg.py:124-129): S = U diag(theta) U^T by
 // parallel cyclic Jacobi (round-robin pairs, k/2 disjoint rotations per
-// round), fp64 S and U; sweeps until the off-diagonal mass is below
-// 1e-30 of the total (relative 1e-15, Frobenius). Output: theta descending and
-// U's columns in that order (jb.m, k x k, ld k). The Ritz blocks after the
-// first filtered iteration are nearly diagonal, so 2-3 sweeps suffice.
-// S lives in shared memory when it fits (k <= 163), else in the global
-// scratch; the accumulated rotation is kept TRANSPOSED (Ut, global scratch,
-// L2-resident) so each rotation updates two contiguous rows (coalesced).
+// round), fp64 S and U; sweeps until the off-diagonal mass is below 1e-30 of
+// the total (relative 1e-15, Frobenius). Output: theta descending and U's
+// columns in that order (jb.m, k x k, ld k).
+// S is kept as its packed upper triangle and the accumulated rotation
+// transposed (Ut: rotations update two contiguous rows), both in shared
+// memory when 8 (k(k+1)/2 + k^2) bytes fit (k <= 132), else in the global
+// scratch. One round = rotation parameters, then every (rotation, rotation)
+// 2x2 block of S updated as J1^T B J2 by one thread (a single pass, no
+// row/column phases) and the Ut rows rotated.
+__device__ __forceinline__ int tri_off(int i, int k) { return i * k - (i * (i - 1)) / 2; }
+__device__ __forceinline__ int tri_idx(int i, int j, int k) {  // symmetric access
+  return i <= j ? tri_off(i, k) + (j - i) : tri_off(j, k) + (i - j);
+}
+
 __global__ void __launch_bounds__(RF_SMALL_THREADS) jacobi_eig_kernel(const SmallJob* __restrict__ jobs) {
   extern __shared__ double rf_smem[];
   __shared__ double red[32];
-  __shared__ int rot_p[256], rot_q[256];
-  __shared__ double rot_c[256], rot_s[256];
+  __shared__ int rot_p[512], rot_q[512];  // k <= 1024
+  __shared__ double rot_c[512], rot_s[512];
   const SmallJob jb = jobs[blockIdx.x];
-  const int k = jb.k, ld = k | 1, tid = threadIdx.x, nt = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  double* S = jb.use_smem ? rf_smem : jb.scratch + (size_t)k * k;
-  double* Ut = jb.scratch;  // k x k, ld k: Ut[c][row] = U[row][c]
-  for (int i = warp; i < k; i += nw)
-    for (int l = lane; l < k; l += 32) {
-      S[i * ld + l] = 0.5 * (jb.g[(size_t)i * k + l] + jb.g[(size_t)l * k + i]);
-      Ut[(size_t)i * k + l] = i == l ? 1.0 : 0.0;
-    }
+  const int k = jb.k, tid = threadIdx.x, nt = blockDim.x;
+  const int ntri = k * (k + 1) / 2;
+  double* S = jb.use_smem ? rf_smem : jb.scratch;
+  double* Ut = S + ((ntri + 1) & ~1);  // k x k, ld k: Ut[c][row] = U[row][c]
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, l = e % k;
+    if (i <= l) S[tri_off(i, k) + (l - i)] = 0.5 * (jb.g[(size_t)i * k + l] + jb.g[(size_t)l * k + i]);
+    Ut[e] = i == l ? 1.0 : 0.0;
+  }
   __syncthreads();
   const int kp = (k + 1) & ~1;
   const int npair = kp / 2;
+  const int nblk = npair * (npair + 1) / 2;
+  // this thread's fixed work items of every round (rotation slots are
+  // positional, so the (i1, i2) block and (rotation, column) maps never change)
+  constexpr int MAXB = 3, MAXU = 9;
+  const bool fast = nblk <= MAXB * nt && npair * k <= MAXU * nt;
+  int bi1[MAXB], bi2[MAXB], ui[MAXU], uc[MAXU];
+  if (fast) {
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) {
+      const int bi = tid + t * nt;
+      bi1[t] = -1;
+      if (bi < nblk) {
+        int i1 = (int)((2.0 * npair + 1.0 - sqrt((2.0 * npair + 1.0) * (2.0 * npair + 1.0) - 8.0 * bi)) * 0.5);
+        while (i1 > 0 && tri_off(i1, npair) > bi) --i1;
+        while (i1 + 1 < npair && tri_off(i1 + 1, npair) <= bi) ++i1;
+        bi1[t] = i1;
+        bi2[t] = i1 + (bi - tri_off(i1, npair));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MAXU; ++t) {
+      const int e = tid + t * nt;
+      ui[t] = e < npair * k ? e / k : -1;
+      uc[t] = e < npair * k ? e % k : 0;
+    }
+  }
+  auto block = [&](int i1, int i2) {
+    const double s1 = rot_s[i1], s2 = rot_s[i2];
+    if (s1 == 0.0 && s2 == 0.0) return;
+    const double c1 = rot_c[i1], c2 = rot_c[i2];
+    const int p1 = rot_p[i1], q1 = rot_q[i1], p2 = rot_p[i2], q2 = rot_q[i2];
+    if (i1 == i2) {  // diagonal block (p, q): becomes diag(app', aqq')
+      const int ip = tri_off(p1, k), iq = tri_off(q1, k), ipq = ip + (q1 - p1);
+      const double app = S[ip], aqq = S[iq], apq = S[ipq];
+      S[ip] = c1 * c1 * app - 2.0 * c1 * s1 * apq + s1 * s1 * aqq;
+      S[iq] = s1 * s1 * app + 2.0 * c1 * s1 * apq + c1 * c1 * aqq;
+      S[ipq] = 0.0;
+      return;
+    }
+    const bool hq1 = q1 < k, hq2 = q2 < k;
+    const int e00 = tri_idx(p1, p2, k);
+    const int e01 = hq2 ? tri_idx(p1, q2, k) : 0;
+    const int e10 = hq1 ? tri_idx(q1, p2, k) : 0;
+    const int e11 = (hq1 && hq2) ? tri_idx(q1, q2, k) : 0;
+    const double b00 = S[e00], b01 = hq2 ? S[e01] : 0.0, b10 = hq1 ? S[e10] : 0.0,
+                 b11 = (hq1 && hq2) ? S[e11] : 0.0;
+    const double x00 = b00 * c2 - b01 * s2, x01 = b00 * s2 + b01 * c2;  // X = B J2
+    const double x10 = b10 * c2 - b11 * s2, x11 = b10 * s2 + b11 * c2;
+    S[e00] = c1 * x00 - s1 * x10;  // J1^T X
+    if (hq2) S[e01] = c1 * x01 - s1 * x11;
+    if (hq1) S[e10] = s1 * x00 + c1 * x10;
+    if (hq1 && hq2) S[e11] = s1 * x01 + c1 * x11;
+  };
+  auto urot = [&](int i, int col) {
+    const double sn = rot_s[i];
+    if (sn == 0.0) return;
+    const double c = rot_c[i];
+    double* up = Ut + (size_t)rot_p[i] * k + col;
+    double* uq = Ut + (size_t)rot_q[i] * k + col;
+    const double a0 = *up, b0 = *uq;
+    *up = c * a0 - sn * b0;
+    *uq = sn * a0 + c * b0;
+  };
   for (int sweep = 0; sweep < 40; ++sweep) {
     double off = 0.0, tot = 0.0;
-    for (int i = warp; i < k; i += nw)
-      for (int l = lane; l < k; l += 32) {
-        const double v = S[i * ld + l] * S[i * ld + l];
-        tot += v;
-        if (i != l) off += v;
+    for (int i = tid >> 5; i < k; i += nt >> 5) {  // a warp per packed row
+      const double* row = S + tri_off(i, k);
+      for (int l = (tid & 31); l < k - i; l += 32) {
+        const double v = row[l] * row[l];
+        tot += l == 0 ? v : 2.0 * v;
+        if (l) off += 2.0 * v;
       }
+    }
     off = blk_sum_d(off, red);
     tot = blk_sum_d(tot, red);
-    if (off <= 1e-30 * tot || tot == 0.0) break;
+    if (off <= jb.tol2 * tot || tot == 0.0) break;
     for (int rd = 0; rd < kp - 1; ++rd) {
       for (int i = tid; i < npair; i += nt) {
         int a, b;
@@ -290,9 +363,10 @@ __global__ void __launch_bounds__(RF_SMALL_THREADS) jacobi_eig_kernel(const Smal
         double c = 1.0, sn = 0.0;
         const int p = min(a, b), q = max(a, b);
         if (q < k) {
-          const double apq = S[p * ld + q];
-          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(S[p * ld + p] * S[q * ld + q]))) {
-            const double tau = (S[q * ld + q] - S[p * ld + p]) / (2.0 * apq);
+          const double apq = S[tri_off(p, k) + (q - p)];
+          const double app = S[tri_off(p, k)], aqq = S[tri_off(q, k)];
+          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+            const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
             sn = t * c;
@@ -301,43 +375,33 @@ __global__ void __launch_bounds__(RF_SMALL_THREADS) jacobi_eig_kernel(const Smal
         rot_p[i] = p; rot_q[i] = q; rot_c[i] = c; rot_s[i] = sn;
       }
       __syncthreads();
-      for (int i = warp; i < npair; i += nw) {  // S <- S J (columns), Ut <- J^T Ut (rows); a warp per rotation
-        const int p = rot_p[i], q = rot_q[i];
-        const double sn = rot_s[i];
-        if (q >= k || sn == 0.0) continue;
-        const double c = rot_c[i];
-        double* up = Ut + (size_t)p * k;
-        double* uq = Ut + (size_t)q * k;
-        for (int row = lane; row < k; row += 32) {
-          const double xp = S[row * ld + p], xq = S[row * ld + q];
-          S[row * ld + p] = c * xp - sn * xq;
-          S[row * ld + q] = sn * xp + c * xq;
-          const double a0 = up[row], b0 = uq[row];
-          up[row] = c * a0 - sn * b0;
-          uq[row] = sn * a0 + c * b0;
+      if (fast) {
+#pragma unroll
+        for (int t = 0; t < MAXB; ++t)
+          if (bi1[t] >= 0) block(bi1[t], bi2[t]);
+#pragma unroll
+        for (int t = 0; t < MAXU; ++t)
+          if (ui[t] >= 0) urot(ui[t], uc[t]);
+      } else {
+        for (int bi = tid; bi < nblk; bi += nt) {
+          int i1 = (int)((2.0 * npair + 1.0 - sqrt((2.0 * npair + 1.0) * (2.0 * npair + 1.0) - 8.0 * bi)) * 0.5);
+          while (i1 > 0 && tri_off(i1, npair) > bi) --i1;
+          while (i1 + 1 < npair && tri_off(i1 + 1, npair) <= bi) ++i1;
+          block(i1, i1 + (bi - tri_off(i1, npair)));
         }
-      }
-      __syncthreads();
-      for (int i = warp; i < npair; i += nw) {  // S <- J^T S (rows)
-        const int p = rot_p[i], q = rot_q[i];
-        const double sn = rot_s[i];
-        if (q >= k || sn == 0.0) continue;
-        const double c = rot_c[i];
-        for (int col = lane; col < k; col += 32) {
-          const double xp = S[p * ld + col], xq = S[q * ld + col];
-          S[p * ld + col] = c * xp - sn * xq;
-          S[q * ld + col] = sn * xp + c * xq;
-        }
+        for (int e = tid; e < npair * k; e += nt) urot(e / k, e % k);
       }
       __syncthreads();
     }
   }
   // descending order; eigenvector i = column i of U = row i of Ut
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  __syncthreads();
   for (int i = warp; i < k; i += nw) {
-    const double ti = S[i * ld + i];
+    const double ti = S[tri_off(i, k)];
     int pos = 0;
     for (int jx = 0; jx < k; ++jx) {
-      const double tj = S[jx * ld + jx];
+      const double tj = S[tri_off(jx, k)];
       pos += (tj > ti) || (tj == ti && jx < i);
     }
     if (lane == 0) jb.theta[pos] = ti;

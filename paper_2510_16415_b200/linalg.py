@@ -29,12 +29,16 @@ __all__ = ["SvdConfig", "check_matrix", "seeded_gaussian", "top_r_right_singular
 _OVERSAMPLE = 4  # linalg.py:94 (the minimum; see oversample_for)
 
 
-def oversample_for(r: int) -> int:
-    """Extra block columns of the converged refresh: the reference carries 4
-    (linalg.py:94); a wider block widens the gap the filter separates
-    (lambda_r vs lambda_k) and cuts the iteration count. Only span(V[:, :r])
-    is returned, so the computed object is unchanged."""
-    return max(_OVERSAMPLE, min(r // 4, 32))
+def oversample_for(r: int, n: int) -> int:
+    """Extra block columns of the converged refresh (Gram dimension n). The
+    reference carries 4 (linalg.py:94). A wider block widens the gap the
+    filter separates (lambda_r vs lambda_k) and cuts the block products, but
+    past k = 132 the device Ritz eigensolve leaves shared memory
+    (csrc/refresh.cuh): measured on B200, 4 is fastest for the 512-wide C1
+    Grams (61 vs 96 ms per refresh) and 32 for the 2048-wide 1B Grams (0.86 vs
+    1.41 s), where the products dominate. Only span(V[:, :r]) is returned, so
+    the computed object is unchanged."""
+    return _OVERSAMPLE if n <= 1024 else max(_OVERSAMPLE, min(r // 4, 32))
 
 
 def seeded_gaussian(rows: int, cols: int, mean: float = 0.0, stddev: float = 1.0, seed: int = 0) -> np.ndarray:
@@ -123,7 +127,7 @@ def refresh_bases(ws: list, ranks: list, svd: SvdConfig, oversample: int | None 
         rows, n = wd.shape
         if not 1 <= r <= n:
             raise ContractViolation(f"rank {r} exceeds the column count of {tuple(wd.shape)}")
-        k = min(n, r + (oversample if oversample is not None else oversample_for(r)))
+        k = min(n, r + (oversample if oversample is not None else oversample_for(r, min(rows, n) if rows >= r + 4 else n)))
         v0 = _start_block64(n, k, svd.seed, dev)
         v1 = torch.empty(n, r, dtype=torch.float32, device=dev)
         v64 = torch.empty(n, r, dtype=torch.float64, device=dev) if want_f64 else None
