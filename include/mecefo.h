@@ -143,6 +143,14 @@ typedef struct {
 const char* mecefo_last_error(void);
 const char* mecefo_version(void);
 
+/* dims->ffn may be any width (model.py:40-61 accepts e.g. LLaMA-1B's 5461):
+ * the engine rounds it up to mecefo_padded_ffn(ffn), a multiple of 8 (16-byte
+ * bf16 rows for TMA). Every ffn-dimensioned buffer the caller passes (W_gate /
+ * W_up rows, W_down columns and row stride, the FFN activations and their
+ * gradients, the down-projection basis rows) uses the padded width with the
+ * pad rows/columns zero — exact: they contribute nothing and their gradients
+ * stay zero. */
+int64_t mecefo_padded_ffn(int64_t ffn);
 int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims);
 int mecefo_engine_destroy(mecefo_engine* e);
 /* Device pointer to the engine's int32 status word (MECEFO_STATUS_* bits);

@@ -161,6 +161,7 @@ _SIGNATURES = {
     "mecefo_last_error": (c_char_p, []),
     "mecefo_version": (c_char_p, []),
     "mecefo_launch_count": (c_int64, []),
+    "mecefo_padded_ffn": (c_int64, [c_int64]),
     "mecefo_engine_create": (c_int, [POINTER(c_void_p), POINTER(Dims)]),
     "mecefo_engine_destroy": (c_int, [c_void_p]),
     "mecefo_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32]),

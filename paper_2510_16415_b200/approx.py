@@ -92,15 +92,16 @@ class ProjectionCache:
                 i = FFN_KINDS.index(kind)
                 v, vt = keep[2 + 2 * i], keep[3 + 2 * i]
                 v.zero_()
-                v[:, :t.shape[1]] = t.to(v.dtype)
+                v[:t.shape[0], :t.shape[1]] = t.to(v.dtype)
                 vt.copy_(v.t())
                 if kind in ("gate", "up") and keep[1] is not None:
                     keep[1][:, i * rp:(i + 1) * rp].copy_(v)
             return
         self._packed.clear()
 
-    def packed(self, precision: str):
-        """Projection struct + keep-alive tensors for the engine."""
+    def packed(self, precision: str, down_rows: int | None = None):
+        """Projection struct + keep-alive tensors for the engine. down_rows:
+        the stored FFN width (V1_down's rows zero-padded to it, model.ffn_storage)."""
         ranks = [int(self.basis[k].shape[1]) for k in FFN_KINDS]
         rp = _pad16(max(ranks))
         key = (precision, rp)
@@ -114,8 +115,9 @@ class ProjectionCache:
             for i, k in enumerate(FFN_KINDS):
                 b = self.basis[k]
                 n_in, r = b.shape
-                v = torch.zeros(n_in, rp, dtype=dt, device=dev)
-                v[:, :r] = b.to(dt)
+                rows = down_rows if (k == "down" and down_rows) else n_in
+                v = torch.zeros(rows, rp, dtype=dt, device=dev)
+                v[:n_in, :r] = b.to(dt)
                 if k in ("gate", "up") and n_in == n_gu:
                     vt = vt_gu[i * rp:(i + 1) * rp]
                     vt.copy_(v.t())
@@ -179,7 +181,7 @@ def backward_block_neighbor(cfg: mdl.ModelConfig, lw: mdl.LayerWeights, cache: m
         if svd is None:
             raise ContractViolation("projection refresh needs an SvdConfig")
         refresh_projections(proj, lw, svd)
-        pst, keep, rp = proj.packed(lw.precision)
+        pst, keep, rp = proj.packed(lw.precision, down_rows=mdl.ffn_storage(cfg))
     dx = torch.empty_like(dy2)
     g = mdl._grad_buffers(cfg, dy2.device, mha=False)
     ws, wn = eng.workspace(b, rp)

@@ -737,11 +737,14 @@ int mecefo_engine_create(mecefo_engine** out, const mecefo_dims* dims) {
   if (d.rope && (d.hidden / d.heads) % 2 != 0) return set_err(MECEFO_ERR_CONTRACT, "rotary positions need an even head dim");
   if (d.precision != MECEFO_PREC_F32 && d.precision != MECEFO_PREC_BF16)
     return set_err(MECEFO_ERR_CONFIG, "unknown precision %d", d.precision);
-  if (d.precision == MECEFO_PREC_BF16 && (d.hidden % 8 != 0 || d.ffn % 8 != 0 || d.vocab % 8 != 0))
-    return set_err(MECEFO_ERR_CONTRACT,
-                   "bf16 (TMA) mode needs hidden, ffn and vocab to be multiples of 8 (16-byte rows); pad ffn");
+  if (d.precision == MECEFO_PREC_BF16 && (d.hidden % 8 != 0 || d.vocab % 8 != 0))
+    return set_err(MECEFO_ERR_CONTRACT, "bf16 (TMA) mode needs hidden and vocab to be multiples of 8 (16-byte rows)");
   auto* e = new mecefo_engine();
   e->d = d;
+  // FFN width padded to 16-byte rows (LLaMA-1B: f = 5461 -> 5464): zero pad
+  // rows of W_gate/W_up and zero pad columns of W_down contribute exactly
+  // nothing forward or backward, and their gradients stay zero.
+  e->d.ffn = mecefo_padded_ffn(d.ffn);
   e->prec = d.precision;
   e->ps = d.precision == MECEFO_PREC_BF16 ? 2 : 4;
   const int hd = (int)(d.hidden / d.heads);
@@ -782,6 +785,8 @@ int mecefo_engine_destroy(mecefo_engine* e) {
   delete e;
   return MECEFO_OK;
 }
+
+int64_t mecefo_padded_ffn(int64_t ffn) { return (ffn + 7) / 8 * 8; }
 
 int mecefo_status_device(mecefo_engine* e, int32_t** out) {
   if (!e || !out) return set_err(MECEFO_ERR_CONTRACT, "null argument");

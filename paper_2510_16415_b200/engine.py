@@ -47,7 +47,7 @@ class StepEngine:
     def __init__(self, cfg: mdl.ModelConfig, precision: str = "bf16", seqs_per_microbatch: int = 32, r: int = 128,
                  tau: int = 100, optim_cfg: op.OptimConfig | None = None, seed: int = 0,
                  weights: mdl.ModelWeights | None = None, svd: SvdConfig | None = None, svd_budgeted: bool = False,
-                 group=None, fuse_lean: bool = True, max_group: int = 2):
+                 group=None, fuse_lean: bool = True, max_group: int = 2, defer_layers: int | None = 4):
         runtime.require_cuda()
         self.cfg = cfg
         self.precision = precision
@@ -88,8 +88,12 @@ class StepEngine:
         # all lean layers at once (grouped launches, mecefo_lowrank_wgrads_batched);
         # each lean layer keeps its output gradient (bf16) and FFN intermediates.
         self.defer_wgrads = precision == "bf16"
-        self._dyc = [None] * (L + 1)
-        self._saved = [None] * L
+        # ... in groups of `defer_layers` consecutive layers (None: all), so
+        # the deferred buffers (h2, act, [d_gate|d_up], dy) exist for at most
+        # that many layers at once (2 b (2m + 3f) bytes per layer)
+        self.defer_layers = L if defer_layers is None else max(1, min(int(defer_layers), L))
+        self._dyc = {}
+        self._saved = {}
         self._ws_lr = None
         self.xf = torch.empty(b, m, dtype=self.dtype, device=self.device)
         self.inv_f = torch.empty(b, **f32)
@@ -160,17 +164,31 @@ class StepEngine:
 
     def _dy_buffer(self, k: int) -> torch.Tensor:
         """Compute-precision gradient of layer k's input (k = L: the head's
-        output), one persistent buffer per layer (the deferred Wgrads read it)."""
-        if self._dyc[k] is None:
-            self._dyc[k] = torch.empty(self.b * self.max_group, self.cfg.hidden, dtype=self.dtype, device=self.device)
-        return self._dyc[k]
+        output). defer_layers + 1 rotating buffers: a deferred Wgrad job of
+        layer l reads dy(l + 1) until its group is flushed."""
+        slot = k % (self.defer_layers + 1)
+        if slot not in self._dyc:
+            self._dyc[slot] = torch.empty(self.b * self.max_group, self.cfg.hidden, dtype=self.dtype,
+                                          device=self.device)
+        return self._dyc[slot]
 
     def _saved_buffers(self, l: int):
-        if self._saved[l] is None:
-            b, m, f = self.b * self.max_group, self.cfg.hidden, self.cfg.ffn_intermediate
+        slot = l % self.defer_layers
+        if slot not in self._saved:
+            b, m, f = self.b * self.max_group, self.cfg.hidden, mdl.ffn_storage(self.cfg)
             mk = lambda n: torch.empty(b, n, dtype=self.dtype, device=self.device)
-            self._saved[l] = (mk(m), mk(f), mk(2 * f))
-        return self._saved[l]
+            self._saved[slot] = (mk(m), mk(f), mk(2 * f))
+        return self._saved[slot]
+
+    def _flush_lowrank(self, jobs: list, b: int, s: int) -> None:
+        """The deferred low-rank FFN Wgrads of a group of lean layers, as
+        grouped launches (mecefo_lowrank_wgrads_batched)."""
+        if not jobs:
+            return
+        arr = (_lib.LowrankJob * len(jobs))(*jobs)
+        wsl, wnl = self._lowrank_ws(b, len(jobs))
+        _lib.call("mecefo_lowrank_wgrads_batched", self.eng.handle, arr, len(jobs), b, wsl, wnl, s)
+        jobs.clear()
 
     def _lowrank_ws(self, b: int, count: int):
         n = int(_lib.load().mecefo_lowrank_batched_workspace_bytes(self.eng.handle, b, self.rp, count))
@@ -233,7 +251,7 @@ class StepEngine:
                 pc.token = lead.token
                 pc.refreshes += 1
                 pc.svd_calls += len(lead.basis)
-        return lead.packed(self.precision)
+        return lead.packed(self.precision, down_rows=mdl.ffn_storage(self.cfg))
 
     def microbatch(self, mb: Microbatch, loss_ptr: int) -> None:
         self._run([mb], loss_ptr)
@@ -276,6 +294,7 @@ class StepEngine:
                   runtime.ptr(dxc(cfg.layers) if defer else self.dx_c[cur]),
                   self._gp("final_norm"), self._gp("unembedding"), mb.alpha_global, b, ws, wn, s)
         jobs, keeps = [], []
+        since_flush = 0
         for l in reversed(range(cfg.layers)):
             nxt = 1 - cur
             dyc_in = dxc(l + 1) if defer else self.dx_c[cur]
@@ -306,10 +325,12 @@ class StepEngine:
                           ctypes.byref(caches[l]), self.dx[cur].data_ptr(), runtime.ptr(dyc_in),
                           self.dx[nxt].data_ptr(), runtime.ptr(dxc_out), ctypes.byref(g), b, ws, wn, s)
             cur = nxt
-        if jobs:  # the deferred low-rank FFN Wgrads of every lean layer, grouped
-            arr = (_lib.LowrankJob * len(jobs))(*jobs)
-            wsl, wnl = self._lowrank_ws(b, len(jobs))
-            _lib.call("mecefo_lowrank_wgrads_batched", eng.handle, arr, len(jobs), b, wsl, wnl, s)
+            since_flush += 1
+            if defer and since_flush == self.defer_layers:  # rotating buffers are about to be reused
+                self._flush_lowrank(jobs, b, s)
+                since_flush = 0
+        if defer:
+            self._flush_lowrank(jobs, b, s)
         self._keep = keeps
         _lib.call("mecefo_embedding_backward", eng.handle, self.tok.data_ptr(), self.dx[cur].data_ptr(),
                   self._gp("embedding"), mb.alpha_global, b, s)
@@ -437,49 +458,85 @@ class StepEngine:
             self._adam_launch(lr, skip, slot, runtime.stream_ptr())
         return self.losses
 
+    def plan_key(self, mbs: list, skip=()) -> tuple:
+        """Identity of an iteration's plan: everything a captured graph bakes
+        in — microbatch ranks, per-layer modes and Eq. (1) weights, input
+        buffers, the skip list, whether the lean microbatches run fused, and
+        the addresses of the projection operands (stable across in-place
+        refreshes, new after an adoption reset)."""
+        ops = []
+        for mb in mbs:
+            for l in range(self.cfg.layers):
+                if mb.lean[l] and (mb.rank, l) in self.projs:
+                    pk = self.projs[(mb.rank, l)]._packed
+                    ops.append(tuple(sorted((k, v[1][2].data_ptr()) for k, v in pk.items())))
+        return (tuple((mb.rank, tuple(mb.lean), tuple(mb.alpha_mha), mb.alpha_ffn, mb.alpha_global,
+                       mb.tokens.data_ptr(), mb.targets.data_ptr()) for mb in mbs), tuple(sorted(skip)),
+                self._fusable(mbs), tuple(ops))
+
+    def has_graph(self, mbs: list, skip=()) -> bool:
+        return self.plan_key(mbs, skip) in getattr(self, "_graph_cache", {})
+
     def capture(self, mbs: list, n_ranks: int, skip=()) -> None:
-        """Capture one whole iteration (both microbatches' forward/backward,
-        the Eq. (1) all-reduce and the fused AdamW) as CUDA graphs, one per
-        optimizer-segment slot. Call after an eager step with the same plan
-        (projections refreshed, descriptors and kernel attributes warm)."""
+        """Capture one whole iteration of this plan (both microbatches'
+        forward/backward, the Eq. (1) all-reduce and the fused AdamW) as CUDA
+        graphs, one per optimizer-segment slot, into a plan-keyed cache (a
+        rotating failure plan reuses its graphs when the plan recurs). Call
+        after an eager step with the same plan (projections refreshed,
+        descriptors and kernel attributes warm)."""
         if self.losses is None or self.losses.numel() != n_ranks:
             self.losses = torch.zeros(n_ranks, dtype=torch.float32, device=self.device)
+        if not hasattr(self, "_graph_cache"):
+            self._graph_cache = {}
+            self._graph_pool = torch.cuda.graph_pool_handle()
         self._seg_slot(0, 0)
         arr, total_numel, names = op.adam_segments(self.weights, self.opt, 1e-4, skip)
-        self._adam_meta = (len(names), total_numel)
-        self._graph_plan = (list(mbs), n_ranks, tuple(skip))
+        meta = (len(names), total_numel)
+        self._adam_meta = meta
         torch.cuda.synchronize()
         steps = {k: pc.step for k, pc in self.projs.items()}
-        self.graphs = []
+        graphs = []
         for slot in range(2):
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, pool=self._graph_pool):
                 self._body(mbs, self.losses)
                 self._adam_launch(0.0, skip, slot, runtime.stream_ptr(), fill=False, record=False)
-            self.graphs.append(g)
+            graphs.append(g)
         for k, v in steps.items():  # capture ran the host bookkeeping once; undo it
             self.projs[k].step = v
         self.iter -= 2
+        key = self.plan_key(mbs, skip)
+        self._graph_cache[key] = (graphs, (list(mbs), n_ranks, tuple(skip)), meta)
+        self._graph_key = key
+        self.graphs = graphs
+        self._graph_plan = (list(mbs), n_ranks, tuple(skip))
         torch.cuda.synchronize()
 
-    def replay(self, lr: float) -> torch.Tensor:
+    def drop_graphs(self) -> None:
+        self._graph_cache = {}
+        self.graphs = []
+
+    def replay(self, lr: float, mbs: list | None = None, skip=()) -> torch.Tensor:
         """One captured iteration: host bookkeeping (optimizer scalars,
-        projection step counters) then a single graph launch."""
+        projection step counters) then a single graph launch. mbs=None
+        replays the most recently captured plan."""
         self.check_status()
-        mbs, n_ranks, skip = self._graph_plan
+        key = self._graph_key if mbs is None else self.plan_key(mbs, skip)
+        graphs, (mbs_c, n_ranks, skip_c), meta = self._graph_cache[key]
+        self._adam_meta = meta
         slot = self._seg_k = (getattr(self, "_seg_k", 0) + 1) % 2
         host, dev, ev = self._segs[slot]
         ev.synchronize()
-        arr, _, names = op.adam_segments(self.weights, self.opt, lr, skip)
+        arr, _, names = op.adam_segments(self.weights, self.opt, lr, skip_c)
         host.numpy()[: arr.nbytes] = arr.view(np.uint8)
         for name in names:
             self.opt.step[name] = self.opt.step.get(name, 0) + 1
-        for mb in mbs:
+        for mb in mbs_c:
             for l in range(self.cfg.layers):
                 if mb.lean[l]:
                     self.proj(mb.rank, l).step += 1
         self.iter += 1
-        self.graphs[slot].replay()
+        graphs[slot].replay()
         ev.record()
         return self.losses
 

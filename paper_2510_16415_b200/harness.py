@@ -334,25 +334,32 @@ def run_training(cfg: RunConfig, out_dir: str | None = None, quiet: bool = True,
 
 # --- weight wire format (harness.py:635-665: final_weights.bin + .json) -----
 
-def pack_weights(layout, master: np.ndarray):
+def pack_weights(layout, master: np.ndarray, cfg: mdl.ModelConfig | None = None):
     """Canonical-order dense little-endian float64 blob + manifest from the
-    aligned flat parameter store (padding between groups dropped)."""
+    aligned flat parameter store (padding between groups — and, given cfg,
+    the FFN-width padding inside gate/up/down — dropped: reference shapes)."""
     params, chunks, off = [], [], 0
     for name, shape, src in layout:
-        n = int(np.prod(shape))
-        params.append({"name": name, "shape": list(shape), "offset_elems": off})
-        chunks.append(master[src: src + n])
+        block = master[src: src + int(np.prod(shape))].reshape(shape)
+        if cfg is not None:
+            block = mdl.logical_view(cfg, name, block)
+        n = block.size
+        params.append({"name": name, "shape": list(block.shape), "offset_elems": off})
+        chunks.append(np.ascontiguousarray(block).reshape(-1))
         off += n
     blob = np.concatenate(chunks).astype("<f8") if chunks else np.zeros(0, "<f8")
     return blob, {"dtype": "<f8", "total_elems": off, "params": params}
 
 
-def unpack_weights(layout, total: int, blob: np.ndarray, manifest: dict) -> np.ndarray:
+def unpack_weights(layout, total: int, blob: np.ndarray, manifest: dict,
+                   cfg: mdl.ModelConfig | None = None) -> np.ndarray:
     """Inverse of pack_weights into an aligned fp32 flat store; names and
-    shapes must match the model's layout (ContractViolation otherwise)."""
+    shapes must match the model's (reference) shapes (ContractViolation
+    otherwise); FFN padding stays zero."""
     from .errors import ContractViolation
 
-    want = {name: (tuple(shape), src) for name, shape, src in layout}
+    want = {name: (tuple(mdl.logical_shape(cfg, name, shape)) if cfg is not None else tuple(shape), shape, src)
+            for name, shape, src in layout}
     host = np.zeros(total, dtype=np.float32)
     seen = set()
     for e in manifest["params"]:
@@ -363,7 +370,11 @@ def unpack_weights(layout, total: int, blob: np.ndarray, manifest: dict) -> np.n
         start = int(e["offset_elems"])
         if start + n > blob.size:
             raise ContractViolation(f"final_weights.bin too short for {name}")
-        host[want[name][1]: want[name][1] + n] = blob[start: start + n]
+        _, sshape, src = want[name]
+        block = host[src: src + int(np.prod(sshape))].reshape(sshape)
+        if cfg is not None:
+            block = mdl.logical_view(cfg, name, block)
+        block[...] = blob[start: start + n].reshape(shape)
         seen.add(name)
     missing = set(want) - seen
     if missing:
@@ -375,7 +386,7 @@ def dump_weights(weights: mdl.ModelWeights, out_dir: str) -> None:
     """harness.py:635-651: one device->host copy of the fp32 master store,
     written as final_weights.bin (<f8, canonical order) + final_weights.json."""
     os.makedirs(out_dir, exist_ok=True)
-    blob, manifest = pack_weights(weights.layout, weights.master.detach().cpu().numpy())
+    blob, manifest = pack_weights(weights.layout, weights.master.detach().cpu().numpy(), weights.cfg)
     tmp = os.path.join(out_dir, "final_weights.bin.tmp")
     blob.tofile(tmp)
     os.replace(tmp, os.path.join(out_dir, "final_weights.bin"))
@@ -390,7 +401,7 @@ def load_weights(cfg: mdl.ModelConfig, out_dir: str, precision: str = "fp32") ->
         manifest = json.load(f)
     blob = np.fromfile(os.path.join(out_dir, "final_weights.bin"), dtype="<f8")
     w = mdl.ModelWeights(cfg, precision)
-    host = unpack_weights(w.layout, w.total, blob, manifest)
+    host = unpack_weights(w.layout, w.total, blob, manifest, cfg)
     w.master.copy_(torch.from_numpy(host).to(w.device))
     w.sync_shadow()
     return w

@@ -10,6 +10,14 @@ canonical order (model.py:35,101-108), each group aligned to 64 elements, so
 q|k|v and gate|up are contiguous (3m, m) and (2f, m) matrices the engine
 reads as single operands. bf16 mode keeps a flat bf16 operand shadow with the
 same offsets, refreshed by the fused AdamW kernel.
+
+The FFN width is stored padded to fp = mecefo_padded_ffn(f) (a multiple of 8,
+16-byte bf16 rows; LLaMA-1B's f = 5461 -> 5464): gate/up are (fp, m) blocks
+whose first f rows are the parameter, down is (m, fp) whose first f columns
+are. The pads are zero and stay zero (zero rows/columns contribute nothing,
+their gradients are zero, AdamW keeps a zero weight at zero), so the step is
+exactly the unpadded one; every reference-facing accessor returns the
+logical (f-wide) view.
 """
 
 from __future__ import annotations
@@ -65,10 +73,42 @@ class ModelConfig:
         return self.hidden // self.heads
 
 
+def ffn_storage(cfg: ModelConfig) -> int:
+    """Stored FFN width (include/mecefo.h mecefo_padded_ffn)."""
+    return (cfg.ffn_intermediate + 7) // 8 * 8
+
+
+def logical_shape(cfg: ModelConfig, name: str, shape: tuple) -> tuple:
+    """The reference's shape of a parameter stored as `shape`."""
+    f, fp = cfg.ffn_intermediate, ffn_storage(cfg)
+    if fp == f or not name.startswith("layers."):
+        return tuple(shape)
+    kind = name.rsplit(".", 1)[1]
+    if kind in ("gate", "up"):
+        return (f, shape[1])
+    if kind == "down":
+        return (shape[0], f)
+    return tuple(shape)
+
+
+def logical_view(cfg: ModelConfig, name: str, storage: torch.Tensor) -> torch.Tensor:
+    """Reference-shaped view of a parameter's storage block (slices off the
+    FFN padding; a strided view for down)."""
+    f, fp = cfg.ffn_intermediate, ffn_storage(cfg)
+    if fp == f or not name.startswith("layers."):
+        return storage
+    kind = name.rsplit(".", 1)[1]
+    if kind in ("gate", "up"):
+        return storage[:f]
+    if kind == "down":
+        return storage[:, :f]
+    return storage
+
+
 def _param_layout(cfg: ModelConfig):
-    """(name, shape, offset) in canonical order; groups aligned to 64 elements,
-    q|k|v and gate|up packed back to back."""
-    m, f, v = cfg.hidden, cfg.ffn_intermediate, cfg.vocab
+    """(name, storage shape, offset) in canonical order; groups aligned to 64
+    elements, q|k|v and gate|up packed back to back; FFN width padded."""
+    m, f, v = cfg.hidden, ffn_storage(cfg), cfg.vocab
     shapes = {"q": (m, m), "k": (m, m), "v": (m, m), "o": (m, m), "norm_mha": (m,), "gate": (f, m), "up": (f, m),
               "down": (m, f), "norm_ffn": (m,)}
     out = []
@@ -146,15 +186,20 @@ class ModelWeights:
                                                                           device=self.device)
         self.layers = [LayerWeights(self, l) for l in range(cfg.layers)]
 
-    # --- reference-style accessors -------------------------------------
-    def named(self):
-        for name, shape, off in self.layout:
-            yield name, self.master[off: off + int(np.prod(shape))].view(shape)
-
-    def get(self, name: str) -> torch.Tensor:
+    # --- reference-style accessors (logical, reference-shaped views) ----
+    def view(self, flat: torch.Tensor, name: str) -> torch.Tensor:
+        """Reference-shaped view of parameter `name` inside any flat buffer
+        with this layout (master weights, gradients, optimizer moments)."""
         off = self.offsets[name]
         shape = self.shapes[name]
-        return self.master[off: off + int(np.prod(shape))].view(shape)
+        return logical_view(self.cfg, name, flat[off: off + int(np.prod(shape))].view(shape))
+
+    def named(self):
+        for name, _, _ in self.layout:
+            yield name, self.view(self.master, name)
+
+    def get(self, name: str) -> torch.Tensor:
+        return self.view(self.master, name)
 
     def set(self, name: str, value) -> None:
         t = torch.as_tensor(np.asarray(value) if not torch.is_tensor(value) else value)
@@ -162,9 +207,7 @@ class ModelWeights:
         self.sync_shadow(name)
 
     def shadow_view(self, name: str) -> torch.Tensor:
-        off = self.offsets[name]
-        shape = self.shapes[name]
-        return self.shadow[off: off + int(np.prod(shape))].view(shape)
+        return self.view(self.shadow, name)
 
     def sync_shadow(self, name: str | None = None) -> None:
         """Refresh the compute-precision operand copy (bf16 mode)."""
@@ -203,6 +246,12 @@ class ModelWeights:
         return {n: t.detach().double().cpu().numpy() for n, t in self.named()}
 
 
+def _host_view(w: "ModelWeights", host: np.ndarray, name: str) -> np.ndarray:
+    off = w.offsets[name]
+    shape = w.shapes[name]
+    return logical_view(w.cfg, name, host[off: off + int(np.prod(shape))].reshape(shape))
+
+
 def init_weights(cfg: ModelConfig, seed: int, std: float = INIT_STD, precision: str = "fp32",
                  device=None) -> ModelWeights:
     """model.py:138-167, bit-identical draws (host PCG64), uploaded once."""
@@ -218,8 +267,7 @@ def init_weights(cfg: ModelConfig, seed: int, std: float = INIT_STD, precision: 
     draws += [("embedding", (v, m)), ("unembedding", (v, m))]
     for name, (r, c) in draws:
         counter += 1
-        off = w.offsets[name]
-        host[off: off + r * c] = seeded_gaussian(r, c, 0.0, std, counter).reshape(-1)
+        _host_view(w, host, name)[...] = seeded_gaussian(r, c, 0.0, std, counter)
     for name, shape, off in w.layout:
         if name.endswith("norm_mha") or name.endswith("norm_ffn") or name == "final_norm":
             host[off: off + shape[0]] = 1.0
@@ -232,8 +280,9 @@ def from_numpy(cfg: ModelConfig, arrays: dict, precision: str = "fp32", device=N
     """Upload reference-layout arrays (e.g. faultsim ModelWeights.named())."""
     w = ModelWeights(cfg, precision, device)
     host = np.zeros(w.total, dtype=np.float32)
-    for name, shape, off in w.layout:
-        host[off: off + int(np.prod(shape))] = np.asarray(arrays[name], dtype=np.float64).reshape(-1)
+    for name, _, _ in w.layout:
+        _host_view(w, host, name)[...] = np.asarray(arrays[name], dtype=np.float64).reshape(
+            logical_shape(cfg, name, w.shapes[name]))
     w.master.copy_(torch.from_numpy(host))
     w.sync_shadow()
     return w
@@ -278,7 +327,7 @@ def _to_2d(cfg: ModelConfig, x: torch.Tensor) -> torch.Tensor:
 
 
 def _alloc_full_cache(cfg: ModelConfig, b: int, dtype, device) -> dict:
-    m, f, H = cfg.hidden, cfg.ffn_intermediate, cfg.heads
+    m, f, H = cfg.hidden, ffn_storage(cfg), cfg.heads
     e = lambda *s, dt=dtype: torch.empty(*s, dtype=dt, device=device)
     return {"h1": e(b, m), "inv1": e(b, dt=torch.float32), "qkv": e(b, 3 * m), "ctx": e(b, m),
             "lse": e(b, H, dt=torch.float32), "h2": e(b, m), "inv2": e(b, dt=torch.float32), "gu": e(b, 2 * f),
@@ -304,7 +353,7 @@ def forward_block(cfg: ModelConfig, lw: LayerWeights, x, mode: str = CACHE_FULL)
 
 
 def _grad_buffers(cfg: ModelConfig, device, mha: bool):
-    m, f = cfg.hidden, cfg.ffn_intermediate
+    m, f = cfg.hidden, ffn_storage(cfg)
     z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)
     g = {"gu": z(2 * f, m), "down": z(m, f), "norm_ffn": z(m)}
     if mha:
@@ -318,8 +367,8 @@ def _grads_struct(g: dict, alpha_mha=1.0, alpha_ffn=1.0) -> _lib.LayerGrads:
 
 
 def _unpack_grads(cfg: ModelConfig, g: dict) -> dict:
-    m, f = cfg.hidden, cfg.ffn_intermediate
-    out = {"gate": g["gu"][:f], "up": g["gu"][f:], "down": g["down"], "norm_ffn": g["norm_ffn"]}
+    m, f, fp = cfg.hidden, cfg.ffn_intermediate, ffn_storage(cfg)
+    out = {"gate": g["gu"][:f], "up": g["gu"][fp:fp + f], "down": g["down"][:, :f], "norm_ffn": g["norm_ffn"]}
     if "qkv" in g:
         out.update({"q": g["qkv"][:m], "k": g["qkv"][m:2 * m], "v": g["qkv"][2 * m:], "o": g["o"],
                     "norm_mha": g["norm_mha"]})
@@ -347,7 +396,7 @@ def ffn_forward(lw: LayerWeights, x1) -> dict:
     cfg = lw.cfg
     x2 = _to_2d(cfg, x1)
     eng = runtime.engine_for(cfg, lw.precision)
-    b, m, f = x2.shape[0], cfg.hidden, cfg.ffn_intermediate
+    b, m, f = x2.shape[0], cfg.hidden, ffn_storage(cfg)
     dt = eng.dtype
     out = {"h2": torch.empty(b, m, dtype=dt, device=x2.device),
            "inv_rms2": torch.empty(b, 1, dtype=torch.float32, device=x2.device),
@@ -359,7 +408,8 @@ def ffn_forward(lw: LayerWeights, x1) -> dict:
               out["inv_rms2"].data_ptr(), out["gate"].data_ptr(), out["up"].data_ptr(), out["act"].data_ptr(),
               out["down"].data_ptr(), ws, wn, runtime.stream_ptr())
     lead = x1.shape[:-1]
-    return {k: v.reshape(*lead, v.shape[-1]) for k, v in out.items()}
+    fl = cfg.ffn_intermediate
+    return {k: (v[:, :fl] if k in ("gate", "up", "act") else v).reshape(*lead, -1) for k, v in out.items()}
 
 
 # ---------------------------------------------------------------------------

@@ -141,15 +141,16 @@ def apply_step(weights, state: OptimState, grads: dict, lr_t: float, skip=()) ->
     names in `skip` keep weights and optimizer state untouched."""
     skip = set(skip)
     flat = torch.zeros(weights.total, dtype=torch.float32, device=weights.master.device)
-    for name, shape, off in weights.layout:
+    for name, _, _ in weights.layout:
         if name in skip:
             continue
         if name not in grads:
             raise ContractViolation(f"missing gradient for {name!r}")
         g = grads[name]
-        if tuple(g.shape) != tuple(shape):
-            raise ContractViolation(f"shape mismatch for {name!r}: {tuple(shape)} vs {tuple(g.shape)}")
-        flat[off: off + int(np.prod(shape))].copy_(torch.as_tensor(g).reshape(-1))
+        dst = weights.view(flat, name)  # reference shape (FFN padding stays zero)
+        if tuple(g.shape) != tuple(dst.shape):
+            raise ContractViolation(f"shape mismatch for {name!r}: {tuple(dst.shape)} vs {tuple(g.shape)}")
+        dst.copy_(torch.as_tensor(g).reshape(dst.shape))
     apply_flat(weights, state, flat, lr_t, skip)
 
 

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import model_ref, optim_ref
-from paper_2510_16415_b200 import _lib, cluster as cl, costmodel as cm
+from paper_2510_16415_b200 import _lib, cluster as cl, costmodel as cm, model as mdl
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "tests", "golden")
@@ -112,3 +112,28 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "_LIB", None)
     with pytest.raises(_lib.EngineUnavailable):
         _lib.load(str(tmp_path / "nope.so"))
+
+
+def test_padded_ffn_layout_and_wire_format_round_trip():
+    """f = 5461 (LLaMA-1B) is stored padded to 5464; the reference-facing
+    views and the final_weights wire format keep the reference's shapes."""
+    from paper_2510_16415_b200 import harness
+
+    cfg = mdl.ModelConfig(vocab=16, hidden=32, heads=4, ffn_intermediate=5461, layers=1, seq_len=8)
+    layout, total = mdl._param_layout(cfg)
+    shapes = {n: s for n, s, _ in layout}
+    assert mdl.ffn_storage(cfg) == 5464
+    assert shapes["layers.0.gate"] == (5464, 32) and shapes["layers.0.down"] == (32, 5464)
+    assert mdl.logical_shape(cfg, "layers.0.down", shapes["layers.0.down"]) == (32, 5461)
+    rng = np.random.default_rng(0)
+    host = np.zeros(total, dtype=np.float32)
+    ref = {}
+    for name, shape, off in layout:
+        blk = mdl.logical_view(cfg, name, host[off: off + int(np.prod(shape))].reshape(shape))
+        ref[name] = rng.normal(size=blk.shape).astype(np.float32)
+        blk[...] = ref[name]
+    blob, manifest = harness.pack_weights(layout, host, cfg)
+    assert [tuple(p["shape"]) for p in manifest["params"]] == [ref[n].shape for n, _, _ in layout]
+    assert blob.size == sum(v.size for v in ref.values())
+    back = harness.unpack_weights(layout, total, blob, manifest, cfg)
+    assert np.array_equal(back, host)  # pads come back as zero
