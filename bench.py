@@ -430,8 +430,9 @@ def run_scenario(args, dims, world, rank, local, group):
     harness.py:382-446 semantics) is driven EVERY iteration; adoptions reset the
     adopted rank's projection caches (harness.py:384-388), which forces a
     converged refresh at its next lean backward. Plans are replayed from a
-    plan-keyed CUDA-graph cache (eager step + capture the first time a plan is
-    seen or when a refresh is due). value = R * 8192 tokens per iteration /
+    plan-keyed CUDA-graph cache (a plan that persists 3 iterations is captured
+    once and replayed whenever it recurs; short-lived plans and iterations
+    with a due refresh launch eagerly). value = R * 8192 tokens per iteration /
     wall time of the whole loop (refreshes, captures and host control plane
     included); time-averaged drop against the fault-free step."""
     import torch
@@ -460,6 +461,7 @@ def run_scenario(args, dims, world, rank, local, group):
     ff_tps = R * job.b * args.steps / (ms_ff / 1000.0)
 
     degraded_iters, refreshes, captures, events_log = 0, 0, 0, []
+    run_len, last_key = 0, None
     job.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -486,15 +488,20 @@ def run_scenario(args, dims, world, rank, local, group):
         failed = [s for s in range(R) if state._st[0, s] == 1]
         degraded_iters += bool(failed)
         mbs, skip = job.plan(failed, job.dev_batches)
+        key = (tuple(failed), len(mbs))
+        run_len = run_len + 1 if key == last_key else 1
+        last_key = key
         if job.eng.projections_due(mbs):
             refreshes += 1
             job.eng.step(mbs, R, job.lr, skip=skip, check=False)
         elif job.eng.has_graph(mbs, skip):
             job.eng.replay(job.lr, mbs, skip)
-        else:
+        elif run_len >= 3:  # a plan that persists: capture it (reused whenever it recurs)
             captures += 1
             job.eng.step(mbs, R, job.lr, skip=skip, check=False)
             job.eng.capture(mbs, R, skip)
+        else:  # short-lived plan: eager launches (a capture costs ~2 host-side iterations)
+            job.eng.step(mbs, R, job.lr, skip=skip, check=False)
     en.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0

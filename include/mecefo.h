@@ -347,6 +347,8 @@ typedef struct mecefo_refresh_job {
   double residual;    /* out (host): final relative residual */
   int32_t products;   /* out (host): block products with W^T W (or W W^T) spent */
   int32_t converged;  /* out (host): 1 if residual <= tol */
+  int32_t rr_steps;   /* out (host): Rayleigh-Ritz steps */
+  int32_t jacobi_sweeps; /* out (host): Jacobi sweeps over all Ritz solves */
 } mecefo_refresh_job;
 
 /* Chebyshev-filtered block subspace iteration with Rayleigh-Ritz, all

@@ -138,6 +138,8 @@ class RefreshJob(ctypes.Structure):
         ("residual", ctypes.c_double),
         ("products", c_int32),
         ("converged", c_int32),
+        ("rr_steps", c_int32),
+        ("jacobi_sweeps", c_int32),
     ]
 
 

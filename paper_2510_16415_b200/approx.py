@@ -74,9 +74,12 @@ class ProjectionCache:
     _packed: dict = field(default_factory=dict, repr=False)
 
     def reset(self) -> None:
+        """Adoption (harness.py:384-388): forget the basis and the step count.
+        The packed engine operands are kept (and overwritten in place by the
+        next refresh) so captured CUDA graphs of recurring plans stay valid."""
+        self._shapes = {k: tuple(v.shape) for k, v in self.basis.items()}
         self.step = 0
         self.basis.clear()
-        self._packed.clear()
         self.token = None
 
     def set_basis(self, kind: str, v1) -> None:
@@ -84,8 +87,9 @@ class ProjectionCache:
         t = torch.as_tensor(v1).to("cuda", torch.float32).contiguous()
         self.token = ("inject", object())
         old = self.basis.get(kind)
+        old_shape = tuple(old.shape) if old is not None else getattr(self, "_shapes", {}).get(kind)
         self.basis[kind] = t
-        if old is not None and tuple(old.shape) == tuple(t.shape):
+        if old_shape == tuple(t.shape) and self._packed:
             # refresh in place: packed engine operands keep their addresses
             # (captured CUDA graphs read them by pointer)
             for (prec, rp), (_, keep) in self._packed.items():

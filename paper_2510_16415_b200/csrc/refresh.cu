@@ -29,6 +29,8 @@
 // max_iterations budget (the reference spends one per iteration).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -44,6 +46,15 @@ namespace {
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 constexpr int kSlots = 96;  // device job-array slots per outer iteration
+// Chebyshev amplification ceiling T_d(x_max) per filtered step:
+// clamp(kChebScale / residual, kChebMin, kChebMax); overridable for experiments
+// through MECEFO_CHEB="min,max,scale".
+double kChebMin = 1e8, kChebMax = 1e12, kChebScale = 1e4;
+struct ChebEnv {
+  ChebEnv() {
+    if (const char* v = getenv("MECEFO_CHEB")) sscanf(v, "%lf,%lf,%lf", &kChebMin, &kChebMax, &kChebScale);
+  }
+} g_cheb_env;
 constexpr size_t kSmemLimit = 227 * 1024;
 
 struct RfPlan {
@@ -56,6 +67,7 @@ struct RfPlan {
   double *G, *Q, *Wq, *GV, *V, *Xa, *Xb, *S, *Mk, *Uk, *scr, *Vs, *BVs, *P;
   int done = 0;
   int products = 0;
+  int rr_steps = 0;
   double resid = INFINITY, tol_inner = 0.0;
   std::vector<double> theta;
 };
@@ -173,7 +185,7 @@ size_t mecefo_refresh_workspace_bytes(const mecefo_refresh_job* jobs, int32_t co
   }
   const size_t slot = al256(2 * (size_t)count * std::max(sizeof(DJob), std::max(sizeof(SmallJob), sizeof(ResJob) + sizeof(CopyJob) + sizeof(AxJob))));
   total += kSlots * slot;
-  total += al256((size_t)count * (kmax + 1) * sizeof(double));
+  total += al256((size_t)count * (kmax + 2) * sizeof(double));
   return total + 1024;
 }
 
@@ -216,7 +228,7 @@ int qr2(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<double*>& Z, std::vector<
       const size_t need = ((size_t)pp->k * (pp->k | 1) + 2 * (size_t)pp->k) * 8;
       const int use = need <= kSmemLimit - 1024 ? 1 : 0;
       if (use) smem = std::max(smem, need);
-      sj.push_back(SmallJob{pp->S, pp->Mk, nullptr, pp->scr, pp->k, use, 0.0});
+      sj.push_back(SmallJob{pp->S, pp->Mk, nullptr, pp->scr, pp->k, use, 0.0, nullptr});
     }
     TRY(run_small(cx, (const void*)cholqr_kernel, sj, smem));
     std::vector<DJob> m;
@@ -247,6 +259,7 @@ int rayleigh_ritz(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<int>& idx) {
     j.M = (int)p.n; j.N = p.k; j.K = (int)p.n;
     a.push_back(j);
     p.products += 1;
+    p.rr_steps += 1;
     DJob s{};
     s.a = p.Q; s.lda = p.k; s.a_kmajor = 0;
     s.b = p.Wq; s.ldb = p.k;
@@ -266,7 +279,8 @@ int rayleigh_ritz(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<int>& idx) {
     // Jacobi accuracy follows the outer residual: early Ritz steps need only
     // a rough rotation (Frobenius off-mass 1e-8 x the residual, squared)
     const double rel = std::min(1e-6, std::max(1e-15, 1e-4 * p.resid));
-    sj.push_back(SmallJob{p.S, p.Uk, cx.summary + (size_t)idx[i] * (cx.kmax + 1), p.scr, p.k, use, rel * rel});
+    double* th = cx.summary + (size_t)idx[i] * (cx.kmax + 2);
+    sj.push_back(SmallJob{p.S, p.Uk, th, p.scr, p.k, use, rel * rel, th + cx.kmax + 1});
   }
   TRY(run_small(cx, (const void*)jacobi_eig_kernel, sj, smem));
   for (auto* pp : ps) {
@@ -286,7 +300,7 @@ int rayleigh_ritz(Ctx& cx, std::vector<RfPlan*>& ps, std::vector<int>& idx) {
   std::vector<ResJob> rj;
   for (size_t i = 0; i < ps.size(); ++i) {
     RfPlan& p = *ps[i];
-    double* th = cx.summary + (size_t)idx[i] * (cx.kmax + 1);
+    double* th = cx.summary + (size_t)idx[i] * (cx.kmax + 2);
     rj.push_back(ResJob{p.V, p.GV, th, th + cx.kmax, (int)p.n, p.k, p.r});
   }
   int rc = MECEFO_OK;
@@ -375,7 +389,8 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
   off += kSlots * cx.slot_bytes;
   cx.summary = reinterpret_cast<double*>(base + off);
   cx.kmax = kmax;
-  std::vector<double> summary((size_t)count * (kmax + 1));
+  std::vector<double> summary((size_t)count * (kmax + 2));
+  CUDA_TRY(cudaMemsetAsync(cx.summary, 0, summary.size() * 8, cx.s));
   for (int i = 0; i < count; ++i) plans[i].tol_inner = plans[i].dual ? tol / 16.0 : tol;
 
   // ---- B = W^T W (primal) or C = W W^T (dual), from the fp32 weights
@@ -445,7 +460,7 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
     for (int i = 0; i < count; ++i) {
       RfPlan& p = plans[i];
       if (p.done) continue;
-      const double* th = summary.data() + (size_t)i * (kmax + 1);
+      const double* th = summary.data() + (size_t)i * (kmax + 2);
       p.resid = th[kmax];
       p.theta.assign(th, th + p.k);
       if (!(th[0] > 0.0)) {  // B == 0 (linalg.py:112-114): first r standard basis vectors
@@ -484,7 +499,7 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
       for (int i : fin_jobs) {
         RfPlan& p = plans[i];
         const mecefo_refresh_job& jb = jobs[i];
-        double* th = cx.summary + (size_t)i * (kmax + 1);
+        double* th = cx.summary + (size_t)i * (kmax + 2);
         if (!p.dual) {
           cj.push_back(CopyJob{jb.v1, p.V, p.r, p.k, jb.v1_f64, nullptr, (int)p.n, p.r, 0});
           continue;
@@ -512,7 +527,7 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
       // theta out for primal jobs and duals
       for (int i : fin_jobs)
         if (jobs[i].theta)
-          CUDA_TRY(cudaMemcpyAsync(jobs[i].theta, cx.summary + (size_t)i * (kmax + 1), (size_t)plans[i].r * 8,
+          CUDA_TRY(cudaMemcpyAsync(jobs[i].theta, cx.summary + (size_t)i * (kmax + 2), (size_t)plans[i].r * 8,
                                    cudaMemcpyDeviceToDevice, cx.s));
       if (!duals.empty()) {
         for (int i : duals) {
@@ -537,7 +552,7 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
         std::vector<double> resd(duals.size());
         for (size_t q = 0; q < duals.size(); ++q) {
           RfPlan& p = plans[duals[q]];
-          rj.push_back(ResJob{p.Vs, p.BVs, cx.summary + (size_t)duals[q] * (kmax + 1), plans[duals[q]].S, (int)jobs[duals[q]].cols,
+          rj.push_back(ResJob{p.Vs, p.BVs, cx.summary + (size_t)duals[q] * (kmax + 2), plans[duals[q]].S, (int)jobs[duals[q]].cols,
                               p.r, p.r});
         }
         int rc = MECEFO_OK;
@@ -586,7 +601,7 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
       // amplification ceiling T_d(x_max): 1e6 while the block is rough, up to
       // 1e10 as the Ritz vectors converge (their contamination x the ratio
       // stays far below the columns' own signal)
-      const double lim = std::max(1e6, std::min(1e10, 1e2 / std::max(p.resid, 1e-30)));
+      const double lim = std::max(kChebMin, std::min(kChebMax, kChebScale / std::max(p.resid, 1e-30)));
       if (xmax > 1.0 + 1e-12 && p.k < p.n) d = (int)std::floor(std::acosh(lim) / std::acosh(xmax));
       if (p.k >= p.n) d = 1;
       d = std::max(1, std::min(d, 24));
@@ -642,6 +657,8 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
   for (int i = 0; i < count; ++i) {
     jobs[i].residual = plans[i].resid;
     jobs[i].products = plans[i].products;
+    jobs[i].rr_steps = plans[i].rr_steps;
+    jobs[i].jacobi_sweeps = (int32_t)summary[(size_t)i * (kmax + 2) + kmax + 1];
     jobs[i].converged = plans[i].done == 1 ? 1 : 0;
     if (plans[i].done != 1) {
       worst = std::max(worst, plans[i].resid);

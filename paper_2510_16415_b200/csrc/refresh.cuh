@@ -159,6 +159,7 @@ struct SmallJob {
   int k;
   int use_smem;
   double tol2;      // jacobi: stop when off-diagonal mass <= tol2 * total (Frobenius^2)
+  double* stat;     // jacobi (optional): += sweeps run
 };
 
 __device__ __forceinline__ double blk_sum_d(double v, double* red) {
@@ -354,7 +355,14 @@ __global__ void __launch_bounds__(RF_SMALL_THREADS) jacobi_eig_kernel(const Smal
     }
     off = blk_sum_d(off, red);
     tot = blk_sum_d(tot, red);
-    if (off <= jb.tol2 * tot || tot == 0.0) break;
+    if (off <= jb.tol2 * tot || tot == 0.0) {
+      if (tid == 0 && jb.stat) *jb.stat += sweep;
+      break;
+    }
+    // threshold Jacobi: a pair whose a_pq^2 is below tol2 * total / k^2 is
+    // not rotated (all such pairs together hold less than the stopping mass),
+    // so the nearly diagonal Ritz blocks of later iterations cost few rotations
+    const double thr2 = jb.tol2 * tot / ((double)k * (double)k);
     for (int rd = 0; rd < kp - 1; ++rd) {
       for (int i = tid; i < npair; i += nt) {
         int a, b;
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(RF_SMALL_THREADS) jacobi_eig_kernel(const Smal
         if (q < k) {
           const double apq = S[tri_off(p, k) + (q - p)];
           const double app = S[tri_off(p, k)], aqq = S[tri_off(q, k)];
-          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+          if (apq * apq > thr2 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);

@@ -132,7 +132,7 @@ def refresh_bases(ws: list, ranks: list, svd: SvdConfig, oversample: int | None 
         v1 = torch.empty(n, r, dtype=torch.float32, device=dev)
         v64 = torch.empty(n, r, dtype=torch.float64, device=dev) if want_f64 else None
         jobs[i] = _lib.RefreshJob(wd.data_ptr(), rows, n, wd.stride(0), r, k, v0.data_ptr(), v1.data_ptr(),
-                                  v64.data_ptr() if v64 is not None else None, None, 0.0, 0, 0)
+                                  v64.data_ptr() if v64 is not None else None, None, 0.0, 0, 0, 0, 0)
         keep += [wd, v0]
         outs.append(v1)
         outs64.append(v64)
@@ -142,8 +142,9 @@ def refresh_bases(ws: list, ranks: list, svd: SvdConfig, oversample: int | None 
     rc = lib.mecefo_refresh_converged(None, jobs, len(ws), float(svd.tolerance), int(svd.max_iterations),
                                       scratch.data_ptr(), nbytes, runtime.stream_ptr())
     if info is not None:
-        info.extend({"residual": jobs[i].residual, "products": jobs[i].products,
-                     "k": jobs[i].k, "converged": bool(jobs[i].converged)} for i in range(len(ws)))
+        info.extend({"residual": jobs[i].residual, "products": jobs[i].products, "k": jobs[i].k,
+                     "converged": bool(jobs[i].converged), "rr_steps": jobs[i].rr_steps,
+                     "jacobi_sweeps": jobs[i].jacobi_sweeps} for i in range(len(ws)))
     if rc == 3:
         worst = max(jobs[i].residual for i in range(len(ws)) if not jobs[i].converged)
         raise SvdConvergenceError(

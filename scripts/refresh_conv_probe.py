@@ -55,8 +55,9 @@ for name in sys.argv[1:] or ["60M"]:
             refresh_bases(mats, [r] * len(mats), svd, info=info, oversample=os_)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+        sw = [i["jacobi_sweeps"] / max(1, i["rr_steps"]) for i in info]
         print(json.dumps({"model": name, "oversample": os_, "matrices": len(mats), "seconds": round(dt, 4),
                           "products_max": max(i["products"] for i in info),
                           "products_mean": sum(i["products"] for i in info) / len(info),
-                          "residual_max": max(i["residual"] for i in info)}), flush=True)
+                          "residual_max": max(i["residual"] for i in info), "rr_steps_max": max(i["rr_steps"] for i in info), "sweeps_per_rr_mean": sum(sw) / len(sw)}), flush=True)
     print(json.dumps(profile(lambda: refresh_bases(mats, [r] * len(mats), svd, oversample=4))), flush=True)
