@@ -61,6 +61,71 @@ int mecefo_pcg64_integers(mecefo_pcg64_t* s, int64_t low, int64_t high, int64_t*
  * Returns MECEFO_CTL_UNRECOVERABLE when some failed member has no adopter. */
 int mecefo_ring_route(int32_t n, const uint8_t* failed, int32_t* executor);
 
+/* ---- The cluster state machine (reference cluster.py:37-271) --------------
+ * ClusterState + FailureScenario: node health (0 healthy, 1 failed, 2 doubled),
+ * executor map, recovery deadlines, the failure stream (PCG64(seed)),
+ * step_cluster = due recoveries (sorted) -> injection -> NDB reassignment ->
+ * invariants. Codes: MECEFO_CTL_CONTRACT (ContractViolation),
+ * MECEFO_CTL_UNRECOVERABLE (UnrecoverableRankError), 3 (ConsistencyError). */
+#define MECEFO_CTL_CONSISTENCY 3
+
+typedef struct mecefo_cluster mecefo_cluster;
+
+typedef struct {
+    int32_t dp, pp, layers;              /* ClusterConfig (cluster.py:37-66) */
+    const int32_t* stage_boundaries;     /* pp + 1 entries, or NULL: round(s * layers / pp) */
+    int32_t kind;                        /* FailureScenario (cluster.py:69-89): 0 none, 1 per_iteration, 2 scheduled */
+    double probability;
+    int32_t recovery_iterations;
+    double failure_interval_s, recovery_time_s;
+    const int32_t* victims;              /* n_victims (rank, stage) pairs, or NULL = every node */
+    int32_t n_victims;
+    uint64_t seed;
+} mecefo_cluster_config;
+
+/* One event of cluster.py:126-133: kind 0 fail, 1 recover (details.fetched_from =
+ * (from_rank, from_stage)), 2 adopt (details.stage, details.fetched_from_rank =
+ * from_rank; node = the adopting node). */
+typedef struct {
+    double time;
+    int32_t iteration, kind;
+    int32_t node_rank, node_stage;
+    int32_t stage;
+    int32_t from_rank, from_stage;
+} mecefo_cluster_event;
+
+int mecefo_cluster_create(mecefo_cluster** out, const mecefo_cluster_config* cfg);
+int mecefo_cluster_destroy(mecefo_cluster* c);
+/* The state arrays (dp x pp, row-major), owned by the cluster; callers may
+ * read and write them between calls (the Python wrapper views them). */
+int mecefo_cluster_arrays(mecefo_cluster* c, int8_t** status, int32_t** executor);
+int mecefo_cluster_rng(mecefo_cluster* c, mecefo_pcg64_t** rng);
+/* next_failure_time: set if `set`, read into `get` if given. */
+int mecefo_cluster_next_failure_time(mecefo_cluster* c, const double* set, double* get);
+/* down_until: the (rank, stage) -> deadline map, ascending node order; *n = its size. */
+int mecefo_cluster_down_until(mecefo_cluster* c, int32_t* nodes, double* until, int32_t cap, int32_t* n);
+int mecefo_cluster_set_down_until(mecefo_cluster* c, int32_t rank, int32_t stage, const double* until);
+/* cluster.py:136-168, 171-173, 176-187, 190-239, 253-271, 242-250. Events are
+ * written to `events` (capacity cap), their count to *n. */
+int mecefo_cluster_inject(mecefo_cluster* c, double sim_time, int32_t iteration, mecefo_cluster_event* events,
+                          int32_t cap, int32_t* n);
+int mecefo_cluster_due_recoveries(mecefo_cluster* c, double sim_time, int32_t iteration, int32_t* nodes,
+                                  int32_t cap, int32_t* n);
+int mecefo_cluster_recover(mecefo_cluster* c, int32_t rank, int32_t stage, double sim_time, int32_t iteration,
+                           mecefo_cluster_event* events, int32_t cap, int32_t* n);
+int mecefo_cluster_reassign(mecefo_cluster* c, double sim_time, int32_t iteration, mecefo_cluster_event* events,
+                            int32_t cap, int32_t* n);
+int mecefo_cluster_validate(const mecefo_cluster* c);
+int mecefo_cluster_step(mecefo_cluster* c, double sim_time, int32_t iteration, mecefo_cluster_event* events,
+                        int32_t cap, int32_t* n);
+
+/* costmodel.py:206-238 iteration_cost on the current state: FLOPs of the
+ * slowest node (worst), its first executing stage, and the total; a healthy
+ * node runs costmodel block_cost MODE_STANDARD per layer, a doubled one
+ * MODE_NEIGHBOR_APPROX (policy_approx) or the naive standard cost. */
+int mecefo_iteration_cost(const mecefo_cluster* c, int64_t hidden, int64_t ffn, int32_t policy_approx, int64_t r,
+                          int64_t tau, int64_t tokens, int64_t* worst, int32_t* worst_stage, int64_t* total);
+
 #ifdef __cplusplus
 }
 #endif

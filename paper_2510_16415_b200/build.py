@@ -85,5 +85,25 @@ def build(force: bool = False, verbose: bool = True) -> str:
     return OUT
 
 
+def build_timing_variant(out: str = os.path.join(HERE, "libmecefo_timing.so")) -> str:
+    """A second library with the timing-experiment knobs compiled in
+    (-DMECEFO_TIMING_KNOBS; never loaded unless MECEFO_LIB points at it)."""
+    objs, procs = [], []
+    for src in [x for x in SOURCES if os.path.exists(os.path.join(CSRC, x))]:
+        obj = os.path.join(CSRC, src.replace(".cu", ".timing.o"))
+        procs.append(subprocess.Popen([nvcc(), *NVCC_FLAGS, "-DMECEFO_TIMING_KNOBS", "-c", "-o", obj,
+                                       os.path.join(CSRC, src)]))
+        objs.append(obj)
+    if any(p_.wait() for p_ in procs):
+        raise subprocess.CalledProcessError(1, "nvcc")
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs], check=True)
+    for o in objs:
+        os.remove(o)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    if "--timing" in sys.argv:
+        build_timing_variant()
+    else:
+        build(force="--force" in sys.argv)

@@ -1,10 +1,11 @@
 """Cluster control plane — drop-in for faultsim.cluster (cluster.py:1-322).
 
 Host-side, replicated identically in every rank process (so skip lists and
-active sets need no communication). State is kept in small integer arrays:
-`_st[i, s]` (0 healthy, 1 failed, 2 doubled) and `_ex[i, s]` (executing
-stage within DP rank i); `status` / `executor` expose the reference's
-dict-of-tuples view. Integer semantics (draw order, recovery-before-
+active sets need no communication). The state machine is native C++
+(libmecefo_ctl.so, include/mecefo_ctl.h: mecefo_cluster_*): the small
+integer arrays `_st[i, s]` (0 healthy, 1 failed, 2 doubled) and `_ex[i, s]`
+(executing stage within DP rank i) are numpy views of its memory;
+`status` / `executor` expose the reference's dict-of-tuples view. Integer semantics (draw order, recovery-before-
 injection, descending-failed NDB takeover with cascading) are bit-exact with
 the reference and tested against its logs (tests/test_cluster_product.py).
 
@@ -16,6 +17,7 @@ Two placements share this module:
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import Iterable
 
@@ -139,19 +141,131 @@ class _ExecutorView:
         return iter([(i, s) for i in range(self._ex.shape[0]) for s in range(self._ex.shape[1])])
 
 
+class _DownUntil:
+    """`ClusterState.down_until` (cluster.py:101): (rank, stage) -> recovery
+    deadline, stored in the native state (mutable-mapping view)."""
+
+    def __init__(self, state: "ClusterState"):
+        self._s = state
+
+    def _items(self) -> list:
+        lib, h = _pcg.load(), self._s._h
+        n = ctypes.c_int32()
+        lib.mecefo_cluster_down_until(h, None, None, 0, ctypes.byref(n))
+        k = n.value
+        nodes = np.zeros(2 * max(k, 1), dtype=np.int32)
+        until = np.zeros(max(k, 1), dtype=np.float64)
+        lib.mecefo_cluster_down_until(h, nodes.ctypes.data, until.ctypes.data, k, ctypes.byref(n))
+        return [((int(nodes[2 * j]), int(nodes[2 * j + 1])), float(until[j])) for j in range(k)]
+
+    def __getitem__(self, node):
+        for k, v in self._items():
+            if k == tuple(node):
+                return v
+        raise KeyError(node)
+
+    def __setitem__(self, node, value):
+        v = ctypes.c_double(float(value))
+        if _pcg.load().mecefo_cluster_set_down_until(self._s._h, int(node[0]), int(node[1]), ctypes.byref(v)):
+            raise ContractViolation(f"node {tuple(node)} outside the cluster")
+
+    def pop(self, node, *default):
+        try:
+            v = self[node]
+        except KeyError:
+            if default:
+                return default[0]
+            raise
+        _pcg.load().mecefo_cluster_set_down_until(self._s._h, int(node[0]), int(node[1]), None)
+        return v
+
+    def __contains__(self, node):
+        return any(k == tuple(node) for k, _ in self._items())
+
+    def __len__(self):
+        return len(self._items())
+
+    def __iter__(self):
+        return iter([k for k, _ in self._items()])
+
+    def items(self):
+        return self._items()
+
+    def keys(self):
+        return [k for k, _ in self._items()]
+
+
+_KIND_CODE = {SCENARIO_NONE: 0, SCENARIO_PER_ITERATION: 1, SCENARIO_SCHEDULED: 2}
+
+
 class ClusterState:
-    """cluster.py:92-123."""
+    """cluster.py:92-123, held by the native state machine (libmecefo_ctl.so,
+    include/mecefo_ctl.h mecefo_cluster_*): `_st` / `_ex` are numpy views of
+    its arrays, `down_until` and `next_failure_time` live there, and the
+    failure stream is its PCG64(seed) (cluster.py:98)."""
+
+    native = True
 
     def __init__(self, cfg: ClusterConfig, scenario: FailureScenario):
         self.cfg = cfg
         self.scenario = scenario
-        # native PCG64 (libmecefo_ctl.so), draw-for-draw == Generator(PCG64(seed)) of cluster.py:98
-        self.rng = Pcg64Generator(scenario.seed)
-        self._st = np.zeros((cfg.dp, cfg.pp), dtype=np.int8)
-        self._ex = np.tile(np.arange(cfg.pp, dtype=np.int32), (cfg.dp, 1))
-        self.down_until: dict = {}
-        self.next_failure_time = scenario.failure_interval_s
+        lib = _pcg.load()
+        bounds = (ctypes.c_int32 * (cfg.pp + 1))(*cfg.boundaries())
+        self._bounds = bounds
+        vic = None
+        nv = 0
+        if scenario.victims is not None:
+            flat = [int(x) for v in scenario.victims for x in v]
+            vic = (ctypes.c_int32 * max(1, len(flat)))(*flat)
+            nv = len(flat) // 2
+        self._vic = vic
+        conf = _pcg.ClusterConfigC(cfg.dp, cfg.pp, cfg.layers, ctypes.cast(bounds, ctypes.c_void_p),
+                                   _KIND_CODE[scenario.kind], float(scenario.probability),
+                                   int(scenario.recovery_iterations), float(scenario.failure_interval_s),
+                                   float(scenario.recovery_time_s),
+                                   ctypes.cast(vic, ctypes.c_void_p) if vic is not None else None, nv,
+                                   int(scenario.seed))
+        h = ctypes.c_void_p()
+        if lib.mecefo_cluster_create(ctypes.byref(h), ctypes.byref(conf)):
+            raise ConfigError("invalid cluster configuration")
+        self._h = h
+        sp, ep = ctypes.c_void_p(), ctypes.c_void_p()
+        lib.mecefo_cluster_arrays(h, ctypes.byref(sp), ctypes.byref(ep))
+        n = cfg.dp * cfg.pp
+        self._st = np.ctypeslib.as_array((ctypes.c_int8 * n).from_address(sp.value)).reshape(cfg.dp, cfg.pp)
+        self._ex = np.ctypeslib.as_array((ctypes.c_int32 * n).from_address(ep.value)).reshape(cfg.dp, cfg.pp)
+        self.down_until = _DownUntil(self)
         self._victims = None if scenario.victims is None else {tuple(v) for v in scenario.victims}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _pcg.load().mecefo_cluster_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
+
+    @property
+    def rng(self) -> Pcg64Generator:
+        """The failure stream (a view of the native PCG64 state)."""
+        p = ctypes.c_void_p()
+        _pcg.load().mecefo_cluster_rng(self._h, ctypes.byref(p))
+        g = Pcg64Generator.__new__(Pcg64Generator)
+        g._s = _pcg._State.from_address(p.value)
+        g._owner = self
+        return g
+
+    @property
+    def next_failure_time(self) -> float:
+        v = ctypes.c_double()
+        _pcg.load().mecefo_cluster_next_failure_time(self._h, None, ctypes.byref(v))
+        return v.value
+
+    @next_failure_time.setter
+    def next_failure_time(self, value: float) -> None:
+        v = ctypes.c_double(float(value))
+        _pcg.load().mecefo_cluster_next_failure_time(self._h, ctypes.byref(v), None)
 
     @property
     def status(self):
@@ -187,57 +301,61 @@ def _event(time, iteration, kind, node, **details) -> dict:
             "details": details}
 
 
+def _native_events(state: ClusterState, fn, *args) -> list:
+    """Call a native cluster entry point and convert its event records to the
+    reference's event dicts (cluster.py:126-133)."""
+    cap = 3 * state.cfg.dp * state.cfg.pp + 16
+    buf = (_pcg.ClusterEventC * cap)()
+    n = ctypes.c_int32()
+    rc = fn(state._h, *args, buf, cap, ctypes.byref(n))
+    out = []
+    for e in buf[: n.value]:
+        node = (e.node_rank, e.node_stage)
+        if e.kind == 0:
+            out.append(_event(e.time, e.iteration, "fail", node))
+        elif e.kind == 1:
+            out.append(_event(e.time, e.iteration, "recover", node, fetched_from=[e.from_rank, e.from_stage]))
+        else:
+            out.append(_event(e.time, e.iteration, "adopt", node, stage=e.stage,
+                              layers=list(state.cfg.layers_of_stage(e.stage)), fetched_from_rank=e.from_rank))
+    if rc == _pcg.MECEFO_CTL_UNRECOVERABLE:
+        failed = {i: sorted(int(s) for s in np.nonzero(state._st[i] == 1)[0]) for i in range(state.cfg.dp)}
+        bad = [i for i, f in failed.items() if f and _pcg.ring_route(state.cfg.pp, f) is None]
+        i = bad[0] if bad else 0
+        raise UnrecoverableRankError(f"DP rank {i}: no eligible adopter for stage (failed stages {failed[i]})")
+    if rc == 3:
+        raise ConsistencyError("cluster state violates the partition / status invariants")
+    if rc:
+        raise ContractViolation("invalid control-plane request")
+    return out
+
+
 def inject_failures(state: ClusterState, scenario: FailureScenario, sim_time: float, iteration: int) -> list:
-    """cluster.py:136-168. Only healthy (and, if listed, victim) nodes draw."""
-    events = []
-    if scenario.kind == SCENARIO_NONE:
-        return events
-    if scenario.kind == SCENARIO_PER_ITERATION:
-        if scenario.probability == 0.0:
-            return events
-        for i, s in state.nodes():
-            if state._st[i, s] != 0:
-                continue
-            if state._victims is not None and (i, s) not in state._victims:
-                continue
-            if state.rng.random() < scenario.probability:
-                state._st[i, s] = 1
-                state.down_until[(i, s)] = iteration + scenario.recovery_iterations
-                events.append(_event(sim_time, iteration, "fail", (i, s)))
-        return events
-    while sim_time >= state.next_failure_time:
-        boundary = state.next_failure_time
-        state.next_failure_time += scenario.failure_interval_s
-        cands = state.healthy_nodes()
-        if state._victims is not None:
-            cands = [n for n in cands if n in state._victims]
-        if not cands:
-            continue
-        node = cands[int(state.rng.integers(len(cands)))]
-        state._st[node] = 1
-        state.down_until[node] = boundary + scenario.recovery_time_s
-        events.append(_event(boundary, iteration, "fail", node))
-    return events
+    """cluster.py:136-168 (native). Only healthy (and, if listed, victim)
+    nodes draw; `scenario` must be the state's own."""
+    if scenario is not state.scenario and scenario != state.scenario:
+        raise ContractViolation("inject_failures: scenario differs from the state's")
+    return _native_events(state, _pcg.load().mecefo_cluster_inject, float(sim_time), int(iteration))
 
 
 def due_recoveries(state: ClusterState, sim_time: float, iteration: int) -> list:
-    """cluster.py:171-173."""
-    clock = iteration if state.scenario.kind == SCENARIO_PER_ITERATION else sim_time
-    return sorted(n for n, until in state.down_until.items() if clock >= until)
+    """cluster.py:171-173 (native)."""
+    lib = _pcg.load()
+    cap = state.cfg.dp * state.cfg.pp
+    nodes = np.zeros(2 * max(cap, 1), dtype=np.int32)
+    n = ctypes.c_int32()
+    lib.mecefo_cluster_due_recoveries(state._h, float(sim_time), int(iteration), nodes.ctypes.data, cap,
+                                      ctypes.byref(n))
+    return [(int(nodes[2 * j]), int(nodes[2 * j + 1])) for j in range(n.value)]
 
 
 def recover_node(state: ClusterState, node, sim_time: float, iteration: int) -> list:
-    """cluster.py:176-187."""
+    """cluster.py:176-187 (native)."""
     i, s = node
-    if state._st[i, s] != 1:
+    if not (0 <= i < state.cfg.dp and 0 <= s < state.cfg.pp) or state._st[i, s] != 1:
         raise ContractViolation(f"node {tuple(node)} is not failed")
-    old = int(state._ex[i, s])
-    state._st[i, s] = 0
-    state.down_until.pop((i, s), None)
-    state._ex[i, s] = s
-    if old != s and state._st[i, old] == 2 and int((state._ex[i] == old).sum()) == 1:
-        state._st[i, old] = 0
-    return [_event(sim_time, iteration, "recover", (i, s), fetched_from=[i, old])]
+    return _native_events(state, lambda h, *a: _pcg.load().mecefo_cluster_recover(h, int(i), int(s), *a),
+                          float(sim_time), int(iteration))
 
 
 def ring_route(n: int, failed) -> list | None:
@@ -250,54 +368,21 @@ def ring_route(n: int, failed) -> list | None:
 
 
 def reassign_takeover(state: ClusterState, sim_time: float = 0.0, iteration: int = 0) -> list:
-    """cluster.py:190-239."""
-    cfg = state.cfg
-    events = []
-    for i in range(cfg.dp):
-        failed = [int(s) for s in np.nonzero(state._st[i] == 1)[0]]
-        route = ring_route(cfg.pp, failed)
-        if route is None:
-            raise UnrecoverableRankError(f"DP rank {i}: no eligible adopter for stage "
-                                         f"(failed stages {sorted(failed)})")
-        adopters = {route[s] for s in failed}
-        for s in range(cfg.pp):
-            if s not in failed:
-                state._ex[i, s] = s
-        for s in sorted(failed, reverse=True):
-            if int(state._ex[i, s]) != route[s]:
-                state._ex[i, s] = route[s]
-                events.append(_event(sim_time, iteration, "adopt", (i, route[s]), stage=s,
-                                     layers=list(cfg.layers_of_stage(s)),
-                                     fetched_from_rank=(i + 1) % cfg.dp if cfg.dp > 1 else i))
-        for s in range(cfg.pp):
-            if s not in failed:
-                state._st[i, s] = 2 if s in adopters else 0
-    return events
+    """cluster.py:190-239 (native): per DP rank, failed stages in descending
+    order take the first ring successor that is neither failed nor adopting."""
+    return _native_events(state, _pcg.load().mecefo_cluster_reassign, float(sim_time), int(iteration))
 
 
 def validate_state(state: ClusterState) -> None:
-    """cluster.py:253-271: partition and status-coupling invariants."""
-    cfg = state.cfg
-    for i in range(cfg.dp):
-        for s in range(cfg.pp):
-            if state._st[i, int(state._ex[i, s])] == 1:
-                raise ConsistencyError(f"stage ({i},{s}) assigned to failed node ({i},{int(state._ex[i, s])})")
-        counts = np.bincount(state._ex[i], minlength=cfg.pp)
-        for s in range(cfg.pp):
-            want = {0: 1, 1: 0, 2: 2}[int(state._st[i, s])]
-            if counts[s] != want:
-                raise ConsistencyError(f"{_NAMES[state._st[i, s]]} node ({i},{s}) executes {counts[s]} stages")
+    """cluster.py:253-271 (native): partition and status-coupling invariants."""
+    if _pcg.load().mecefo_cluster_validate(state._h):
+        raise ConsistencyError("cluster state violates the partition / status invariants")
 
 
 def step_cluster(state: ClusterState, sim_time: float, iteration: int) -> list:
-    """cluster.py:242-250: recoveries, then failures, then reassignment."""
-    events = []
-    for node in due_recoveries(state, sim_time, iteration):
-        events.extend(recover_node(state, node, sim_time, iteration))
-    events.extend(inject_failures(state, state.scenario, sim_time, iteration))
-    events.extend(reassign_takeover(state, sim_time, iteration))
-    validate_state(state)
-    return events
+    """cluster.py:242-250 (native): recoveries, then failures, then
+    reassignment, then the invariants — one call into libmecefo_ctl.so."""
+    return _native_events(state, _pcg.load().mecefo_cluster_step, float(sim_time), int(iteration))
 
 
 def active_set(state: ClusterState, layer: int, kind: str) -> list:

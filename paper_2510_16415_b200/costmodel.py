@@ -46,8 +46,27 @@ def block_flops(cfg, mode: str, r: int, tau: int, tokens: int) -> int:
 
 
 def iteration_cost(state: cl.ClusterState, model_cfg, policy: str, r: int, tau: int, tokens_per_rank: int):
-    """costmodel.py:206-238: (worst node flops, its first stage, total, 0).
-    Activation bytes are not tracked here (the 4th value is always 0)."""
+    """costmodel.py:206-238: (worst node flops, its first stage, total, 0),
+    computed natively on the cluster state (mecefo_iteration_cost,
+    libmecefo_ctl.so). Activation bytes are not tracked here (always 0)."""
+    import ctypes
+
+    from . import pcg
+
+    worst, stage, total = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
+    rc = pcg.load().mecefo_iteration_cost(state._h, int(model_cfg.hidden), int(model_cfg.ffn_intermediate),
+                                          1 if policy == POLICY_APPROX else 0, int(r), int(tau),
+                                          int(tokens_per_rank), ctypes.byref(worst), ctypes.byref(stage),
+                                          ctypes.byref(total))
+    if rc:
+        from .errors import ContractViolation
+
+        raise ContractViolation("iteration_cost: invalid arguments")
+    return worst.value, stage.value, total.value, 0
+
+
+def iteration_cost_py(state: cl.ClusterState, model_cfg, policy: str, r: int, tau: int, tokens_per_rank: int):
+    """The same accounting in Python (cross-check of the native version)."""
     cfg = state.cfg
     doubled = MODE_NEIGHBOR_APPROX if policy == POLICY_APPROX else MODE_NEIGHBOR_NAIVE
     per_mode = {}

@@ -212,3 +212,357 @@ int mecefo_ring_route(int32_t n, const uint8_t* failed, int32_t* executor) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The cluster state machine (reference cluster.py:92-271): node health,
+// executor map, recovery deadlines, failure injection (per-iteration coin
+// flips or scheduled interval crossings on the simulated clock), ring-successor
+// NDB reassignment and the partition invariants — and iteration_cost
+// (costmodel.py:206-238), whose FLOP total drives the simulated clock that
+// scheduled failures key on (harness.py:442-446). Mirrors the Python control
+// plane that is replayed bit-exactly against the reference's own logs.
+// ---------------------------------------------------------------------------
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <new>
+#include <vector>
+
+struct mecefo_cluster {
+    int32_t dp = 0, pp = 0, layers = 0;
+    std::vector<int32_t> bounds;        // pp + 1 stage boundaries
+    int32_t kind = 0;                   // 0 none, 1 per_iteration, 2 scheduled
+    double probability = 0.0;
+    int32_t recovery_iterations = 1;
+    double failure_interval_s = 0.0, recovery_time_s = 0.0;
+    bool has_victims = false;
+    std::vector<uint8_t> victim;        // dp * pp
+    mecefo_pcg64_t rng{};
+    std::vector<int8_t> st;             // 0 healthy, 1 failed, 2 doubled
+    std::vector<int32_t> ex;            // executing stage within the DP rank
+    std::map<int32_t, double> down_until;  // node index i * pp + s -> deadline (iteration or sim time)
+    double next_failure_time = 0.0;
+};
+
+namespace {
+
+struct EventSink {
+    mecefo_cluster_event* out;
+    int32_t cap, n;
+    int push(const mecefo_cluster_event& e) {
+        if (n >= cap) return MECEFO_CTL_CONTRACT;
+        out[n++] = e;
+        return MECEFO_CTL_OK;
+    }
+};
+
+mecefo_cluster_event make_event(double t, int32_t it, int32_t kind, int32_t i, int32_t s) {
+    mecefo_cluster_event e{};
+    e.time = t;
+    e.iteration = it;
+    e.kind = kind;
+    e.node_rank = i;
+    e.node_stage = s;
+    e.stage = -1;
+    e.from_rank = -1;
+    e.from_stage = -1;
+    return e;
+}
+
+// cluster.py:136-168 (only healthy, victim-eligible nodes draw; p == 0 draws nothing)
+int inject(mecefo_cluster* c, double sim_time, int32_t iteration, EventSink& ev) {
+    if (c->kind == 0) return MECEFO_CTL_OK;
+    if (c->kind == 1) {
+        if (c->probability == 0.0) return MECEFO_CTL_OK;
+        for (int32_t i = 0; i < c->dp; ++i)
+            for (int32_t s = 0; s < c->pp; ++s) {
+                const int32_t n = i * c->pp + s;
+                if (c->st[n] != 0) continue;
+                if (c->has_victims && !c->victim[n]) continue;
+                double u;
+                mecefo_pcg64_random(&c->rng, &u, 1);
+                if (u < c->probability) {
+                    c->st[n] = 1;
+                    c->down_until[n] = (double)iteration + c->recovery_iterations;
+                    if (ev.push(make_event(sim_time, iteration, 0, i, s))) return MECEFO_CTL_CONTRACT;
+                }
+            }
+        return MECEFO_CTL_OK;
+    }
+    while (sim_time >= c->next_failure_time) {
+        const double boundary = c->next_failure_time;
+        c->next_failure_time += c->failure_interval_s;
+        std::vector<int32_t> cands;
+        for (int32_t n = 0; n < c->dp * c->pp; ++n)  // row-major == sorted (i, s)
+            if (c->st[n] == 0 && (!c->has_victims || c->victim[n])) cands.push_back(n);
+        if (cands.empty()) continue;
+        int64_t pick;
+        mecefo_pcg64_integers(&c->rng, 0, (int64_t)cands.size(), &pick, 1);
+        const int32_t n = cands[(size_t)pick];
+        c->st[n] = 1;
+        c->down_until[n] = boundary + c->recovery_time_s;
+        if (ev.push(make_event(boundary, iteration, 0, n / c->pp, n % c->pp))) return MECEFO_CTL_CONTRACT;
+    }
+    return MECEFO_CTL_OK;
+}
+
+// cluster.py:176-187
+int recover(mecefo_cluster* c, int32_t i, int32_t s, double sim_time, int32_t iteration, EventSink& ev) {
+    const int32_t n = i * c->pp + s;
+    if (c->st[n] != 1) return MECEFO_CTL_CONTRACT;
+    const int32_t old = c->ex[n];
+    c->st[n] = 0;
+    c->down_until.erase(n);
+    c->ex[n] = s;
+    if (old != s && c->st[i * c->pp + old] == 2) {
+        int32_t cnt = 0;
+        for (int32_t t = 0; t < c->pp; ++t) cnt += c->ex[i * c->pp + t] == old;
+        if (cnt == 1) c->st[i * c->pp + old] = 0;
+    }
+    mecefo_cluster_event e = make_event(sim_time, iteration, 1, i, s);
+    e.from_rank = i;
+    e.from_stage = old;
+    return ev.push(e);
+}
+
+// cluster.py:190-239 (descending failed-stage order, ring successor, cascading)
+int reassign(mecefo_cluster* c, double sim_time, int32_t iteration, EventSink& ev) {
+    std::vector<uint8_t> failed(c->pp);
+    std::vector<int32_t> route(c->pp);
+    for (int32_t i = 0; i < c->dp; ++i) {
+        for (int32_t s = 0; s < c->pp; ++s) failed[s] = c->st[i * c->pp + s] == 1;
+        if (mecefo_ring_route(c->pp, failed.data(), route.data()) != MECEFO_CTL_OK) return MECEFO_CTL_UNRECOVERABLE;
+        std::vector<uint8_t> adopter(c->pp, 0);
+        for (int32_t s = 0; s < c->pp; ++s)
+            if (failed[s]) adopter[route[s]] = 1;
+        for (int32_t s = 0; s < c->pp; ++s)
+            if (!failed[s]) c->ex[i * c->pp + s] = s;
+        for (int32_t s = c->pp - 1; s >= 0; --s) {
+            if (!failed[s] || c->ex[i * c->pp + s] == route[s]) continue;
+            c->ex[i * c->pp + s] = route[s];
+            mecefo_cluster_event e = make_event(sim_time, iteration, 2, i, route[s]);
+            e.stage = s;
+            e.from_rank = c->dp > 1 ? (i + 1) % c->dp : i;
+            if (ev.push(e)) return MECEFO_CTL_CONTRACT;
+        }
+        for (int32_t s = 0; s < c->pp; ++s)
+            if (!failed[s]) c->st[i * c->pp + s] = adopter[s] ? 2 : 0;
+    }
+    return MECEFO_CTL_OK;
+}
+
+// cluster.py:253-271
+int validate(const mecefo_cluster* c) {
+    for (int32_t i = 0; i < c->dp; ++i) {
+        std::vector<int32_t> counts(c->pp, 0);
+        for (int32_t s = 0; s < c->pp; ++s) {
+            const int32_t e = c->ex[i * c->pp + s];
+            if (e < 0 || e >= c->pp || c->st[i * c->pp + e] == 1) return 3;
+            counts[e]++;
+        }
+        for (int32_t s = 0; s < c->pp; ++s) {
+            const int8_t v = c->st[i * c->pp + s];
+            const int32_t want = v == 0 ? 1 : (v == 1 ? 0 : 2);
+            if (counts[s] != want) return 3;
+        }
+    }
+    return MECEFO_CTL_OK;
+}
+
+// costmodel.py:103-139 totals (linear layers) and :47-64
+int64_t svd_flops(int64_t m, int64_t n, int64_t r) {
+    const int64_t k = std::min(n, r + 4);
+    return 2 * m * n * n + 30 * (2 * n * n * k + 2 * n * k * k);
+}
+
+int64_t block_flops(int64_t m, int64_t f, int32_t approx, int64_t r, int64_t tau, int64_t b) {
+    const int64_t mats[7][2] = {{m, m}, {m, m}, {m, m}, {m, m}, {f, m}, {f, m}, {m, f}};
+    int64_t total = 0;
+    for (auto& a : mats) total += 2 * b * a[0] * a[1];  // Fprop
+    if (!approx) {
+        for (auto& a : mats) total += 2 * (2 * b * a[0] * a[1]);  // Wgrad + Dgrad
+        return total;
+    }
+    for (int q = 4; q < 7; ++q) {
+        const int64_t a = mats[q][0], c = mats[q][1], re = std::min(r, c);
+        total += 2 * b * a * c * 2;                          // Rcomp + Dgrad
+        total += 2 * re * (b * c + b * a + a * c);           // projected Wgrad
+        total += svd_flops(a, c, re) / tau;                  // amortised SVD
+    }
+    return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mecefo_cluster_create(mecefo_cluster** out, const mecefo_cluster_config* cfg) {
+    if (!out || !cfg || cfg->dp < 1 || cfg->pp < 1 || cfg->layers < cfg->pp) return MECEFO_CTL_CONTRACT;
+    if (cfg->kind < 0 || cfg->kind > 2 || cfg->recovery_iterations < 1) return MECEFO_CTL_CONTRACT;
+    auto* c = new (std::nothrow) mecefo_cluster();
+    if (!c) return MECEFO_CTL_CONTRACT;
+    c->dp = cfg->dp;
+    c->pp = cfg->pp;
+    c->layers = cfg->layers;
+    c->bounds.resize(cfg->pp + 1);
+    for (int32_t s = 0; s <= cfg->pp; ++s)  // round(s * L / pp), Python round-half-even (cluster.py:59-62)
+        c->bounds[s] = cfg->stage_boundaries ? cfg->stage_boundaries[s]
+                                             : (int32_t)std::nearbyint((double)s * cfg->layers / cfg->pp);
+    c->kind = cfg->kind;
+    c->probability = cfg->probability;
+    c->recovery_iterations = cfg->recovery_iterations;
+    c->failure_interval_s = cfg->failure_interval_s;
+    c->recovery_time_s = cfg->recovery_time_s;
+    c->victim.assign((size_t)cfg->dp * cfg->pp, 0);
+    c->has_victims = cfg->victims != nullptr;
+    for (int32_t v = 0; c->has_victims && v < cfg->n_victims; ++v) {
+        const int32_t i = cfg->victims[2 * v], s = cfg->victims[2 * v + 1];
+        if (i >= 0 && i < cfg->dp && s >= 0 && s < cfg->pp) c->victim[(size_t)i * cfg->pp + s] = 1;
+    }
+    const uint64_t seed = cfg->seed;
+    mecefo_pcg64_seed(&c->rng, &seed, 1);
+    c->st.assign((size_t)cfg->dp * cfg->pp, 0);
+    c->ex.resize((size_t)cfg->dp * cfg->pp);
+    for (int32_t i = 0; i < cfg->dp; ++i)
+        for (int32_t s = 0; s < cfg->pp; ++s) c->ex[(size_t)i * cfg->pp + s] = s;
+    c->next_failure_time = cfg->failure_interval_s;
+    *out = c;
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_destroy(mecefo_cluster* c) {
+    delete c;
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_arrays(mecefo_cluster* c, int8_t** status, int32_t** executor) {
+    if (!c || !status || !executor) return MECEFO_CTL_CONTRACT;
+    *status = c->st.data();
+    *executor = c->ex.data();
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_rng(mecefo_cluster* c, mecefo_pcg64_t** rng) {
+    if (!c || !rng) return MECEFO_CTL_CONTRACT;
+    *rng = &c->rng;
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_next_failure_time(mecefo_cluster* c, const double* set, double* get) {
+    if (!c) return MECEFO_CTL_CONTRACT;
+    if (set) c->next_failure_time = *set;
+    if (get) *get = c->next_failure_time;
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_down_until(mecefo_cluster* c, int32_t* nodes, double* until, int32_t cap, int32_t* n) {
+    if (!c || !n) return MECEFO_CTL_CONTRACT;
+    *n = (int32_t)c->down_until.size();
+    int32_t k = 0;
+    for (auto& kv : c->down_until) {
+        if (k >= cap) break;
+        if (nodes) { nodes[2 * k] = kv.first / c->pp; nodes[2 * k + 1] = kv.first % c->pp; }
+        if (until) until[k] = kv.second;
+        ++k;
+    }
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_set_down_until(mecefo_cluster* c, int32_t i, int32_t s, const double* until) {
+    if (!c || i < 0 || i >= c->dp || s < 0 || s >= c->pp) return MECEFO_CTL_CONTRACT;
+    if (until) c->down_until[i * c->pp + s] = *until;
+    else c->down_until.erase(i * c->pp + s);
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_inject(mecefo_cluster* c, double sim_time, int32_t iteration, mecefo_cluster_event* events,
+                          int32_t cap, int32_t* n) {
+    if (!c || !n) return MECEFO_CTL_CONTRACT;
+    EventSink ev{events, cap, 0};
+    const int rc = inject(c, sim_time, iteration, ev);
+    *n = ev.n;
+    return rc;
+}
+
+int mecefo_cluster_due_recoveries(mecefo_cluster* c, double sim_time, int32_t iteration, int32_t* nodes,
+                                  int32_t cap, int32_t* n) {
+    if (!c || !n) return MECEFO_CTL_CONTRACT;
+    const double clock = c->kind == 1 ? (double)iteration : sim_time;
+    int32_t k = 0;
+    for (auto& kv : c->down_until)  // std::map: ascending node index == sorted (i, s)
+        if (clock >= kv.second) {
+            if (k < cap && nodes) { nodes[2 * k] = kv.first / c->pp; nodes[2 * k + 1] = kv.first % c->pp; }
+            ++k;
+        }
+    *n = k;
+    return MECEFO_CTL_OK;
+}
+
+int mecefo_cluster_recover(mecefo_cluster* c, int32_t i, int32_t s, double sim_time, int32_t iteration,
+                           mecefo_cluster_event* events, int32_t cap, int32_t* n) {
+    if (!c || !n || i < 0 || i >= c->dp || s < 0 || s >= c->pp) return MECEFO_CTL_CONTRACT;
+    EventSink ev{events, cap, 0};
+    const int rc = recover(c, i, s, sim_time, iteration, ev);
+    *n = ev.n;
+    return rc;
+}
+
+int mecefo_cluster_reassign(mecefo_cluster* c, double sim_time, int32_t iteration, mecefo_cluster_event* events,
+                            int32_t cap, int32_t* n) {
+    if (!c || !n) return MECEFO_CTL_CONTRACT;
+    EventSink ev{events, cap, 0};
+    const int rc = reassign(c, sim_time, iteration, ev);
+    *n = ev.n;
+    return rc;
+}
+
+int mecefo_cluster_validate(const mecefo_cluster* c) { return c ? validate(c) : MECEFO_CTL_CONTRACT; }
+
+int mecefo_cluster_step(mecefo_cluster* c, double sim_time, int32_t iteration, mecefo_cluster_event* events,
+                        int32_t cap, int32_t* n) {
+    if (!c || !n) return MECEFO_CTL_CONTRACT;
+    EventSink ev{events, cap, 0};
+    const double clock = c->kind == 1 ? (double)iteration : sim_time;
+    std::vector<int32_t> due;
+    for (auto& kv : c->down_until)
+        if (clock >= kv.second) due.push_back(kv.first);
+    int rc = MECEFO_CTL_OK;
+    for (int32_t node : due)
+        if ((rc = recover(c, node / c->pp, node % c->pp, sim_time, iteration, ev))) break;
+    if (!rc) rc = inject(c, sim_time, iteration, ev);
+    if (!rc) rc = reassign(c, sim_time, iteration, ev);
+    if (!rc) rc = validate(c);
+    *n = ev.n;
+    return rc;
+}
+
+int mecefo_iteration_cost(const mecefo_cluster* c, int64_t hidden, int64_t ffn, int32_t policy_approx, int64_t r,
+                          int64_t tau, int64_t tokens, int64_t* worst, int32_t* worst_stage, int64_t* total) {
+    if (!c || !worst || !worst_stage || !total || tau < 1) return MECEFO_CTL_CONTRACT;
+    const int64_t std_f = block_flops(hidden, ffn, 0, r, tau, tokens);
+    const int64_t dbl_f = block_flops(hidden, ffn, policy_approx ? 1 : 0, r, tau, tokens);
+    *worst = 0;
+    *worst_stage = 0;
+    *total = 0;
+    for (int32_t i = 0; i < c->dp; ++i)
+        for (int32_t node = 0; node < c->pp; ++node) {
+            int64_t layers = 0;
+            int32_t first = -1;
+            for (int32_t s = 0; s < c->pp; ++s)
+                if (c->ex[i * c->pp + s] == node) {
+                    layers += c->bounds[s + 1] - c->bounds[s];
+                    if (first < 0) first = s;
+                }
+            if (first < 0) continue;
+            const int64_t fl = layers * (c->st[i * c->pp + node] == 0 ? std_f : dbl_f);
+            *total += fl;
+            if (fl > *worst) {
+                *worst = fl;
+                *worst_stage = first;
+            }
+        }
+    return MECEFO_CTL_OK;
+}
+
+}  // extern "C"

@@ -602,6 +602,9 @@ int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const vo
   p.tiles_n = (int)((f + D2_NP - 1) / D2_NP);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.has_act = act ? 1 : 0;
+#ifdef MECEFO_TIMING_KNOBS
+  if (const char* v = getenv("MECEFO_DUAL_DBG")) p.dbg = atoi(v);
+#endif
   TRY(ensure_smem((const void*)swiglu_bwd_dual128_kernel, D2_SMEM));
   CUDA_TRY(pdl_launch(swiglu_bwd_dual128_kernel, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), D2_SMEM, s,
                       tdy, th2, twd, twgu128, tact, tdg, tdu, p));

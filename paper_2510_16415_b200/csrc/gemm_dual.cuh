@@ -29,6 +29,8 @@ struct DualDev {
   int64_t f_off;    // row offset of W_up inside W_gu (= f)
   int kblocks, tiles_m, tiles_n, num_tiles;
   int has_act;
+  int dbg;  // timing experiments only (MECEFO_TIMING_KNOBS builds): 1 = epilogue skips math/stores,
+            // 2 = gate|up product does not wait for the previous epilogue (results invalid)
 };
 
 // ---------------------------------------------------------------------------
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t bD = (3 * it) & 3, bG = (3 * it + 1) & 3, bU = (3 * it + 2) & 3;
         for (int ph = 0; ph < 2; ++ph) {
           // d-phase reuses the block tile it-2 held; gu-phase the blocks of tile it-1
-          const int need = it - 2 + ph;
+          const int need = (p.dbg & 2) ? -1 : it - 2 + ph;
           while (seen <= need) {
             mbar_wait(edone, seen & 1);
             ++seen;
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_arrive(edone);
         }
         const int n0 = nt * D2_NP + c * 32;
-        if (n0 < p.NP) {
+        if (n0 < p.NP && !(p.dbg & 1)) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float sg = sigmoid_ieee_f(g[j]);

@@ -31,8 +31,37 @@ SYMBOLS = {
     "mecefo_pcg64_random": [ctypes.c_void_p, POINTER(c_double), c_size_t],
     "mecefo_pcg64_integers": [ctypes.c_void_p, c_int64, c_int64, POINTER(c_int64), c_size_t],
     "mecefo_ring_route": [c_int32, POINTER(ctypes.c_uint8), POINTER(c_int32)],
+    "mecefo_cluster_create": [POINTER(ctypes.c_void_p), ctypes.c_void_p],
+    "mecefo_cluster_destroy": [ctypes.c_void_p],
+    "mecefo_cluster_arrays": [ctypes.c_void_p, POINTER(ctypes.c_void_p), POINTER(ctypes.c_void_p)],
+    "mecefo_cluster_rng": [ctypes.c_void_p, POINTER(ctypes.c_void_p)],
+    "mecefo_cluster_next_failure_time": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+    "mecefo_cluster_down_until": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, c_int32, POINTER(c_int32)],
+    "mecefo_cluster_set_down_until": [ctypes.c_void_p, c_int32, c_int32, ctypes.c_void_p],
+    "mecefo_cluster_inject": [ctypes.c_void_p, c_double, c_int32, ctypes.c_void_p, c_int32, POINTER(c_int32)],
+    "mecefo_cluster_due_recoveries": [ctypes.c_void_p, c_double, c_int32, ctypes.c_void_p, c_int32,
+                                      POINTER(c_int32)],
+    "mecefo_cluster_recover": [ctypes.c_void_p, c_int32, c_int32, c_double, c_int32, ctypes.c_void_p, c_int32,
+                               POINTER(c_int32)],
+    "mecefo_cluster_reassign": [ctypes.c_void_p, c_double, c_int32, ctypes.c_void_p, c_int32, POINTER(c_int32)],
+    "mecefo_cluster_validate": [ctypes.c_void_p],
+    "mecefo_cluster_step": [ctypes.c_void_p, c_double, c_int32, ctypes.c_void_p, c_int32, POINTER(c_int32)],
+    "mecefo_iteration_cost": [ctypes.c_void_p, c_int64, c_int64, c_int32, c_int64, c_int64, c_int64,
+                              POINTER(c_int64), POINTER(c_int32), POINTER(c_int64)],
 }
 MECEFO_CTL_UNRECOVERABLE = 2
+
+
+class ClusterConfigC(ctypes.Structure):
+    _fields_ = [("dp", c_int32), ("pp", c_int32), ("layers", c_int32), ("stage_boundaries", ctypes.c_void_p),
+                ("kind", c_int32), ("probability", c_double), ("recovery_iterations", c_int32),
+                ("failure_interval_s", c_double), ("recovery_time_s", c_double), ("victims", ctypes.c_void_p),
+                ("n_victims", c_int32), ("seed", c_uint64)]
+
+
+class ClusterEventC(ctypes.Structure):
+    _fields_ = [("time", c_double), ("iteration", c_int32), ("kind", c_int32), ("node_rank", c_int32),
+                ("node_stage", c_int32), ("stage", c_int32), ("from_rank", c_int32), ("from_stage", c_int32)]
 
 
 class _State(ctypes.Structure):

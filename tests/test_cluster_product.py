@@ -191,3 +191,28 @@ def test_ring_plan_eq1_weights():
     assert a_mha == pytest.approx(1 / 6) and skip == []
     with pytest.raises(UnrecoverableRankError):
         ring_plan(2, {0, 1}, 2)
+
+
+def test_control_plane_is_native_and_matches_python_accounting():
+    """step_cluster / inject / recover / reassign / validate run in the native
+    state machine (libmecefo_ctl.so); iteration_cost's native FLOP accounting
+    equals the Python restatement on random degraded states."""
+    import numpy as np
+
+    from paper_2510_16415_b200 import costmodel as cm, model as mdl
+
+    assert cl.ClusterState.native
+    mcfg = mdl.ModelConfig(vocab=64, hidden=128, heads=4, ffn_intermediate=344, layers=8, seq_len=64)
+    rng = np.random.default_rng(3)
+    for trial in range(40):
+        dp, pp = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+        state = make_state(dp=dp, pp=pp, layers=8, kind="per_iteration", probability=0.3, recovery_iterations=2,
+                           seed=trial)
+        for it in range(6):
+            try:
+                cl.step_cluster(state, 0.0, it)
+            except UnrecoverableRankError:
+                break
+            for policy in (cm.POLICY_APPROX, cm.POLICY_NAIVE):
+                args = (state, mcfg, policy, 32, 100, 256)
+                assert cm.iteration_cost(*args) == cm.iteration_cost_py(*args)
