@@ -578,6 +578,13 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
   return MECEFO_OK;
 }
 
+// Which fused recompute kernel runs: 2 = the CTA-pair (cta_group::2) kernel,
+// 1 = the single-CTA kernel. MECEFO_DUAL=1 selects the latter.
+int dual_variant() {
+  static const int v = getenv("MECEFO_DUAL") ? atoi(getenv("MECEFO_DUAL")) : 2;
+  return v == 1 ? 1 : 2;
+}
+
 // Fused d_act / gate / up tcgen05 kernel + SwiGLU backward epilogue (bf16).
 int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const void* w_down_c, const void* w_gu_c,
                     void* act, void* dcat, int64_t b, cudaStream_t s) {
@@ -602,9 +609,42 @@ int swiglu_bwd_dual(mecefo_engine* e, const void* dy_c, const void* h2, const vo
   p.tiles_n = (int)((f + D2_NP - 1) / D2_NP);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.has_act = act ? 1 : 0;
+  p.act = reinterpret_cast<__nv_bfloat16*>(act);
+  p.dcat = reinterpret_cast<__nv_bfloat16*>(dcat);
+  int variant = dual_variant();
 #ifdef MECEFO_TIMING_KNOBS
   if (const char* v = getenv("MECEFO_DUAL_DBG")) p.dbg = atoi(v);
+  if (const char* v = getenv("MECEFO_DUAL_DIRECT")) p.direct = atoi(v);
 #endif
+  if (variant == 2) {  // CTA-pair kernel: 256-row tiles, B operand halves per CTA
+    CUtensorMap twg64;
+    TRY(make_tmap(e, &twg64, w_gu_c, m, 2 * f, m, 64, 64));
+    p.tiles_m = (int)((b + 2 * TC_BM - 1) / (2 * TC_BM));
+    p.num_tiles = p.tiles_m * p.tiles_n;
+    int epw = 8;  // measured: 16 one-chunk warps spill at 96 registers and lose an operand stage (92.5 vs 86 us)
+#ifdef MECEFO_TIMING_KNOBS
+    if (const char* v = getenv("MECEFO_DUAL_EPW")) epw = atoi(v) == 8 ? 8 : 16;
+#endif
+    auto kern = epw == 16 ? swiglu_bwd_dual2sm_kernel<16> : swiglu_bwd_dual2sm_kernel<8>;
+    const int smem = epw == 16 ? D2S<16>::SMEM : D2S<8>::SMEM;
+    TRY(ensure_smem((const void*)kern, smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * std::min(p.num_tiles, kNumSMs / 2)));
+    cfg.blockDim = dim3(epw == 16 ? D2S<16>::THREADS : D2S<8>::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tdy, th2, twd, twg64, tact, tdg, tdu, p));
+    return check_launch("swiglu_bwd_dual2sm_kernel");
+  }
   TRY(ensure_smem((const void*)swiglu_bwd_dual128_kernel, D2_SMEM));
   CUDA_TRY(pdl_launch(swiglu_bwd_dual128_kernel, dim3(std::min(p.num_tiles, kNumSMs)), dim3(TC_THREADS), D2_SMEM, s,
                       tdy, th2, twd, twgu128, tact, tdg, tdu, p));

@@ -29,6 +29,10 @@ struct DualDev {
   int64_t f_off;    // row offset of W_up inside W_gu (= f)
   int kblocks, tiles_m, tiles_n, num_tiles;
   int has_act;
+  // direct epilogue stores (no smem staging): act (ld f) and [d_gate | d_up] (ld 2f)
+  __nv_bfloat16* act;
+  __nv_bfloat16* dcat;
+  int direct;
   int dbg;  // timing experiments only (MECEFO_TIMING_KNOBS builds): 1 = epilogue skips math/stores,
             // 2 = gate|up product does not wait for the previous epilogue (results invalid)
 };
@@ -44,6 +48,59 @@ struct DualDev {
 // product waits for that epilogue. Stages alternate d-phase (dy + W_down
 // slice) and gu-phase (h2 + gate|up rows) k-blocks.
 // ---------------------------------------------------------------------------
+// 32 fp32 values -> bf16, up to `cnt` columns at p (16-byte vectors when whole).
+__device__ __forceinline__ void store_row32_bf16(__nv_bfloat16* p, const float* v, int cnt) {
+  uint32_t w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    w[j] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  if (cnt == 32 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      reinterpret_cast<uint4*>(p)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < cnt) p[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+// SwiGLU backward of one element (model.py:198-204, 216, 250-253), ~11
+// instructions: s = sigmoid(g) by MUFU ex2 + rcp.approx, gs = silu(g),
+//   act = gs u,  d_up = d gs,  d_gate = d u s (1 + g (1 - s)) = d u (s + gs - gs s).
+// In: g = gate, u = up, d = d_act; out: g = d_gate, u = d_up, d = act.
+__device__ __forceinline__ void swiglu_bwd_elem(float& g, float& u, float& d) {
+  const float s = rcp_approx(1.f + ex2_approx(-1.4426950408889634f * g));
+  const float gs = g * s;
+  const float du = d * gs;
+  const float dg = (d * u) * (s + fmaf(-gs, s, gs));
+  d = gs * u;
+  g = dg;
+  u = du;
+}
+
+// A 32 x 32 bf16 box (lane = row, v = its 32 columns) stored through the
+// warp's 2 KB staging box with coalesced 16-byte st.global (8 rows x 64 B per
+// instruction): no TMA-unit round trip and no completion waits — the box is
+// reused after a warp barrier. gp points at (row 0, column 0) of the box,
+// ld in elements; rows >= rows_left and columns >= cnt (a multiple of 8) are
+// not written.
+__device__ __forceinline__ void stage_store32_lsu(uint8_t* box, const float* v, __nv_bfloat16* gp, int64_t ld,
+                                                  int rows_left, int cnt, int lane) {
+  stage_write16(box, v, PREC_BF16, 0, lane);
+  stage_write16(box, v + 16, PREC_BF16, 1, lane);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = k * 32 + lane, row = q >> 2, u = q & 3;
+    const uint4 w = *reinterpret_cast<const uint4*>(box + row * 64 + ((u ^ ((row >> 1) & 3)) << 4));
+    if (row < rows_left && u * 8 < cnt) *reinterpret_cast<uint4*>(gp + row * ld + u * 8) = w;
+  }
+  __syncwarp();
+}
+
 constexpr int D2_NP = 128;
 constexpr int D2_STAGE_BYTES = TC_BM * TC_BK * 2 + 2 * D2_NP * TC_BK * 2;  // 16 KB A + 32 KB B (max of the phases)
 constexpr int D2_STAGES = 4;
@@ -186,19 +243,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int n0 = nt * D2_NP + c * 32;
         if (n0 < p.NP && !(p.dbg & 1)) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float sg = sigmoid_ieee_f(g[j]);
-            const float act = g[j] * sg * u[j];
-            const float dg = (d[j] * u[j]) * (sg * (1.f + g[j] * (1.f - sg)));
-            const float du = d[j] * (g[j] * sg);
-            g[j] = dg;
-            u[j] = du;
-            d[j] = act;
+          for (int j = 0; j < 32; ++j) swiglu_bwd_elem(g[j], u[j], d[j]);
+          if (p.direct == 2) {  // coalesced LSU stores through the staging box
+            const int64_t f = p.NP;
+            const int cnt = min(32, p.NP - n0), rl = p.M - r0;
+            if (p.has_act) stage_store32_lsu(stg, d, p.act + (int64_t)r0 * f + n0, f, rl, cnt, lane);
+            stage_store32_lsu(stg, g, p.dcat + (int64_t)r0 * 2 * f + n0, 2 * f, rl, cnt, lane);
+            stage_store32_lsu(stg, u, p.dcat + (int64_t)r0 * 2 * f + f + n0, 2 * f, rl, cnt, lane);
+          } else if (p.direct) {  // each lane's row segment of 32 bf16 straight to global (no smem traffic)
+            const int row = r0 + lane;
+            if (row < p.M) {
+              const int64_t f = p.NP;
+              if (p.has_act) store_row32_bf16(p.act + (int64_t)row * f + n0, d, min(32, p.NP - n0));
+              store_row32_bf16(p.dcat + (int64_t)row * 2 * f + n0, g, min(32, p.NP - n0));
+              store_row32_bf16(p.dcat + (int64_t)row * 2 * f + f + n0, u, min(32, p.NP - n0));
+            }
+          } else {
+            // three bf16 boxes through the warp's two 2 KB staging halves (measured 2% faster here)
+            if (p.has_act) stage_store32_db(stg, sb, &tmAct, d, n0, r0, lane);
+            stage_store32_db(stg, sb, &tmDg, g, n0, r0, lane);
+            stage_store32_db(stg, sb, &tmDu, u, n0, r0, lane);
           }
-          // three bf16 boxes through the warp's two 2 KB staging halves (measured 2% faster here)
-          if (p.has_act) stage_store32_db(stg, sb, &tmAct, d, n0, r0, lane);
-          stage_store32_db(stg, sb, &tmDg, g, n0, r0, lane);
-          stage_store32_db(stg, sb, &tmDu, u, n0, r0, lane);
         }
       }
     }
@@ -210,6 +275,247 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
+  }
+}
+
+}  // namespace mecefo
+
+namespace mecefo {
+
+// ---------------------------------------------------------------------------
+// CTA-pair (cta_group::2) variant. A cluster of 2 CTAs computes a 256-token x
+// 128-pair-column tile with M = 256 tcgen05 MMAs issued by the leader CTA:
+// each CTA stages its own 128 rows of dy / h2 (A) but only HALF of the B
+// operand — W_down columns [64 crank, 64 crank + 64) of the tile, and gate /
+// up rows [64 crank, 64 crank + 64) — which the pair's tensor cores share.
+// Per SM that cuts the shared-memory traffic of a k-block (TMA fill + MMA
+// operand read) from 64 + 96 KB to 48 + 64 KB; the measured mainloop-only
+// time of the single-CTA kernel (70 of 92 us at C1) is bound there.
+// TMEM per CTA (its 128 rows): gate|up of the tile in columns [0, 256) as ONE
+// N = 256 product — [g 0-63 | u 0-63] from the leader's B half, [g 64-127 |
+// u 64-127] from the peer's — and d_act in [256, 384) or [384, 512)
+// alternating, so the d_act product of tile i+1 runs under tile i's
+// epilogue. Barriers: stage `full` lives in the leader (both CTAs' TMA bytes
+// land there), `empty` / `tfull` in both (multicast commits), `edone` in the
+// leader (16 epilogue-warp arrivals, 8 of them remote).
+// ---------------------------------------------------------------------------
+constexpr int D2S_STAGE_BYTES = TC_BM * TC_BK * 2 + D2_NP * TC_BK * 2;  // 16 KB A + 16 KB B half (gu-phase)
+// EPW epilogue warps: 8 (two 32-column chunks each, 6 operand stages) or 16
+// (one chunk each: a warp loads its chunk's d_act / gate / up from TMEM and
+// releases the tile's TMEM right away, so the next tile's gate|up product is
+// not held up by the SwiGLU math and stores; 5 operand stages).
+template <int EPW>
+struct D2S {
+  static constexpr int STAGES = EPW == 16 ? 5 : 6;
+  static constexpr int THREADS = 128 + 32 * EPW;
+  static constexpr int SMEM = STAGES * D2S_STAGE_BYTES + EPW * TC_STAGE_OUT + 1024 + 256;
+};
+
+__device__ __forceinline__ void tc_mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the LEADER's barrier
+// (the cta-rank bit of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
+template <int EPW>
+__global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
+    swiglu_bwd_dual2sm_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmH2,
+                              const __grid_constant__ CUtensorMap tmWd, const __grid_constant__ CUtensorMap tmWg,
+                              const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmDg,
+                              const __grid_constant__ CUtensorMap tmDu, DualDev p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int D2S_STAGES = D2S<EPW>::STAGES;
+  uint8_t* sE = smem + D2S_STAGES * D2S_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + EPW * TC_STAGE_OUT);
+  uint64_t* empty = full + D2S_STAGES;
+  uint64_t* tfull = empty + D2S_STAGES;
+  uint64_t* edone = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(edone + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < D2S_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(edone, 2 * EPW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {  // the pair's TMEM, allocated by the same warp of both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote signal
+  griddep_wait();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer (both CTAs) =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs) {
+        const int mt = t % p.tiles_m, nt = t / p.tiles_m;
+        const int row0 = mt * 2 * TC_BM + (int)crank * TC_BM;
+        for (int ph = 0; ph < 2; ++ph) {
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = smem + stage * D2S_STAGE_BYTES;
+            const int k0 = kb * TC_BK;
+            const bool skipA = (p.dbg & 4) && nt != 0;  // timing experiment: A re-reads elided
+            if (ph == 0) {  // dy rows + this CTA's 64 W_down columns (MN-major)
+              if (leader) mbar_expect_tx(&full[stage], 2 * ((skipA ? 0 : TC_BM * TC_BK * 2) + 64 * TC_BK * 2));
+              if (!skipA) tma_load_2d_2sm(st, &tmDy, &full[stage], k0, row0);
+              tma_load_2d_2sm(st + 16384, &tmWd, &full[stage], nt * D2_NP + (int)crank * 64, k0);
+            } else {        // h2 rows + this CTA's 64 gate rows and 64 up rows (K-major)
+              if (leader) mbar_expect_tx(&full[stage], 2 * D2S_STAGE_BYTES - (skipA ? 2 * TC_BM * TC_BK * 2 : 0));
+              if (!skipA) tma_load_2d_2sm(st, &tmH2, &full[stage], k0, row0);
+              tma_load_2d_2sm(st + 16384, &tmWg, &full[stage], k0, nt * D2_NP + (int)crank * 64);
+              tma_load_2d_2sm(st + 16384 + 8192, &tmWg, &full[stage], k0,
+                              (int)p.f_off + nt * D2_NP + (int)crank * 64);
+            }
+            if (++stage == D2S_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ===== MMA issuer (leader CTA only) =====
+      constexpr uint32_t id_d = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((128u >> 3) << 17) |
+                                ((256u >> 4) << 24);  // M = 256, N = 128, B MN-major
+      constexpr uint32_t id_gu = (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int seen = 0;
+      int it = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs, ++it) {
+        const uint32_t dcol = 256u + 128u * (uint32_t)(it & 1);
+        for (int ph = 0; ph < 2; ++ph) {
+          const int need = (p.dbg & 2) ? -1 : it - 2 + ph;  // d: tile it-2 freed this block; gu: tile it-1
+          while (seen <= need) {
+            mbar_wait(edone, seen & 1);
+            ++seen;
+          }
+          tc_fence_after();
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t st = smem_u32(smem + stage * D2S_STAGE_BYTES);
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k) {
+              const uint32_t acc_on = (kb > 0 || k > 0) ? 1u : 0u;
+              const uint64_t ad = make_sdesc(st + k * 32, 16, 1024);
+              if (ph == 0)
+                tc_mma_bf16_2sm(tmem_base + dcol, ad, make_sdesc(st + 16384 + k * 2048, 8192, 1024), id_d, acc_on);
+              else
+                tc_mma_bf16_2sm(tmem_base, ad, make_sdesc(st + 16384 + k * 32, 16, 1024), id_gu, acc_on);
+            }
+            tc_commit_2sm_mc(&empty[stage], 0x3);
+            if (++stage == D2S_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+        tc_commit_2sm_mc(tfull, 0x3);
+      }
+    }
+  } else if (warp >= 4) {  // ===== epilogue (both CTAs) =====
+    const int ew = warp - 4, quad = ew & 3;
+    constexpr int CPW = 16 / EPW;  // 32-column chunks per warp (4 per quadrant, EPW / 4 warps per quadrant)
+    const int cbase = (ew >> 2) * CPW;
+    uint8_t* stg = sE + ew * TC_STAGE_OUT;
+    int sb = 0;
+    int it = 0;
+    for (int t = pair; t < p.num_tiles; t += npairs, ++it) {
+      const int mt = t % p.tiles_m, nt = t / p.tiles_m;
+      const uint32_t dcol = 256u + 128u * (uint32_t)(it & 1);
+      mbar_wait(tfull, it & 1);
+      tc_fence_after();
+      const int r0 = mt * 2 * TC_BM + (int)crank * TC_BM + quad * 32;
+      const uint32_t lanes = tmem_base + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+      for (int cc = 0; cc < CPW; ++cc) {
+        const int c = cbase + cc;
+        const uint32_t gcol = (uint32_t)((c >> 1) * 128 + (c & 1) * 32), ucol = gcol + 64u;
+        float d[32], g[32], u[32];
+        tmem_ld16_nowait(lanes + dcol + c * 32, d);
+        tmem_ld16_nowait(lanes + dcol + c * 32 + 16, d + 16);
+        tmem_ld16_nowait(lanes + gcol, g);
+        tmem_ld16_nowait(lanes + gcol + 16, g + 16);
+        tmem_ld16_nowait(lanes + ucol, u);
+        tmem_ld16_nowait(lanes + ucol + 16, u + 16);
+        tmem_wait_ld();
+        if (cc == CPW - 1) {  // this warp's TMEM reads of the tile are done: release to the leader's MMA
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(edone, 0);
+        }
+        const int n0 = nt * D2_NP + c * 32;
+        if (n0 < p.NP && r0 < p.M && !(p.dbg & 1)) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) swiglu_bwd_elem(g[j], u[j], d[j]);
+          if (p.direct == 2) {  // coalesced LSU stores through the staging box
+            const int64_t f = p.NP;
+            const int cnt = min(32, p.NP - n0), rl = p.M - r0;
+            if (p.has_act) stage_store32_lsu(stg, d, p.act + (int64_t)r0 * f + n0, f, rl, cnt, lane);
+            stage_store32_lsu(stg, g, p.dcat + (int64_t)r0 * 2 * f + n0, 2 * f, rl, cnt, lane);
+            stage_store32_lsu(stg, u, p.dcat + (int64_t)r0 * 2 * f + f + n0, 2 * f, rl, cnt, lane);
+          } else {
+            // three bf16 32x32 boxes through the warp's double-buffered staging (TMA clips rows >= M)
+            if (p.has_act) stage_store32_db(stg, sb, &tmAct, d, n0, r0, lane);
+            stage_store32_db(stg, sb, &tmDg, g, n0, r0, lane);
+            stage_store32_db(stg, sb, &tmDu, u, n0, r0, lane);
+          }
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the pair is done with TMEM and every remote barrier
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
   }
 }
 
