@@ -297,7 +297,8 @@ class Job:
                else SvdConfig(rank=args.rank, tolerance=1e-9, max_iterations=3000, seed=23))
         self.eng = E.StepEngine(self.cfg, precision=args.precision, seqs_per_microbatch=SEQS, r=args.rank, tau=TAU,
                                 seed=0, svd=svd, svd_budgeted=args.budgeted_refresh, group=group,
-                                defer_layers=args.defer_layers)
+                                defer_layers=args.defer_layers, grad_comm=args.grad_comm,
+                                overlap_comm=not args.no_overlap)
         self.lib = _lib.load()
         self.host_batches, self.dev_batches = {}, {}
         for j in range(self.R):
@@ -543,6 +544,10 @@ def main():
     ap.add_argument("--fail-prob", type=float, default=0.03)
     ap.add_argument("--defer-layers", type=int, default=4,
                     help="lean layers whose low-rank Wgrads are grouped (bounds the deferred buffers)")
+    ap.add_argument("--grad-comm", default="fp32", choices=["fp32", "bf16"],
+                    help="dtype of the Eq. (1) gradient all-reduce buckets")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="all-reduce the gradient buckets on the compute stream (no overlap with backward)")
     ap.add_argument("--budgeted-refresh", action="store_true",
                     help="30-iteration budgeted projection refresh instead of the converged one")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -687,6 +692,28 @@ def main():
     h2d = sum(2 * mb.tokens.numel() * 8 for mb in degraded_e2e)
     loss_ok = bool(torch.isfinite(eng.losses).all().item())
 
+    exchange = None
+    if group is not None:  # the Eq. (1) all-reduce alone: NCCL bus bandwidth of the whole flat buffer
+        nbytes = eng.grad.numel() * (2 if args.grad_comm == "bf16" else 4)
+        buf = eng.grad if args.grad_comm == "fp32" else torch.empty(eng.grad.numel(), dtype=torch.bfloat16,
+                                                                     device="cuda")
+        for _ in range(3):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        job.barrier()
+        st_, en_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st_.record()
+        for _ in range(10):
+            dist.all_reduce(buf)
+        en_.record()
+        torch.cuda.synchronize()
+        t_ar = job.max_over_ranks(st_.elapsed_time(en_) / 10)
+        exchange = {"mode": ("bucketed, overlapped with backward on a communication stream"
+                             if not args.no_overlap else "bucketed, on the compute stream"),
+                    "dtype": args.grad_comm, "bytes": nbytes, "buckets": 2 + -(-cfg.layers // args.defer_layers),
+                    "allreduce_whole_buffer_ms": round(t_ar, 3),
+                    "busbw_gbs": round(2 * (world - 1) / world * nbytes / (t_ar / 1e3) / 1e9, 1)}
+
     memory = None
     if world == 1 and not args.no_memory:
         eng.drop_graphs()
@@ -736,7 +763,8 @@ def main():
         "profiled_kernel_ms_per_step": round(kernel_ms / args.steps, 3),
         "gpu_busy_frac_eager": round(kernel_ms / ms_prof, 4),
         "ms_per_step_eager_profiled": round(ms_prof / args.steps, 3),
-        "launch_mode": "cuda_graph" if use_graph else "eager", "memory": memory, "cpu_baseline": cpu,
+        "launch_mode": "cuda_graph" if use_graph else "eager", "exchange": exchange, "memory": memory,
+        "cpu_baseline": cpu,
         "clocks": clk.summary(), "loss_finite": loss_ok, "wall_s_timed": round(wall, 3),
     }
     print(json.dumps(out), flush=True)

@@ -249,6 +249,12 @@ int mecefo_scale_accumulate(const float* src, float* out, int64_t n, float alpha
 /* fp32 -> compute-precision copy (weights' operand shadows). */
 int mecefo_cast(mecefo_engine* e, const float* src, void* dst, int64_t n, void* stream);
 
+/* Gradient exchange in bf16 (cluster.py:292-322 Eq. (1) on the wire): the
+ * pre-weighted fp32 bucket -> bf16 before the all-reduce, and the reduced
+ * bf16 bucket -> fp32 for the optimizer. */
+int mecefo_cast_bf16(const float* src, void* dst_bf16, int64_t n, void* stream);
+int mecefo_widen_bf16(const void* src_bf16, float* dst, int64_t n, void* stream);
+
 /* optim.py:55-57 _check_grad as a device flag: flag[0] |= any(!isfinite(v)). */
 int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream);
 

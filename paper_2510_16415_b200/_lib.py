@@ -223,6 +223,8 @@ _SIGNATURES = {
     "mecefo_scale_accumulate": (c_int, [c_void_p, c_void_p, c_int64, c_float, c_float, c_void_p]),
     "mecefo_cast": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "mecefo_nonfinite": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "mecefo_cast_bf16": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "mecefo_widen_bf16": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "mecefo_adamw_step": (
         c_int,
         [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_float,

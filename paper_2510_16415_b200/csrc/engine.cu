@@ -1539,6 +1539,27 @@ int mecefo_cast(mecefo_engine* e, const float* src, void* dst, int64_t n, void* 
   return cast_to_compute(e, src, dst, n, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int mecefo_cast_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  if (n <= 0) return MECEFO_OK;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  ProfScope prof("grad.cast_bf16", 0.0, 6.0 * n, s);
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8 * kNumSMs);
+  CUDA_TRY(pdl_launch(cast_f32_kernel, dim3((unsigned)blocks), dim3(256), 0, s, src, dst, n, (int)PREC_BF16));
+  return check_launch("cast_f32_kernel");
+}
+
+int mecefo_widen_bf16(const void* src, float* dst, int64_t n, void* stream) {
+  if (n <= 0) return MECEFO_OK;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return set_err(MECEFO_ERR_CONTRACT, "widen_bf16 needs 16-byte aligned buffers");
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  ProfScope prof("grad.widen_bf16", 0.0, 6.0 * n, s);
+  const int64_t blocks = std::min<int64_t>((n / 8 + 255) / 256 + 1, 8 * kNumSMs);
+  CUDA_TRY(pdl_launch(widen_bf16_kernel, dim3((unsigned)blocks), dim3(256), 0, s,
+                      reinterpret_cast<const __nv_bfloat16*>(src), dst, n));
+  return check_launch("widen_bf16_kernel");
+}
+
 int mecefo_nonfinite(const float* v, int64_t n, int32_t* flag, void* stream) {
   if (n <= 0) return MECEFO_OK;
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8 * kNumSMs);

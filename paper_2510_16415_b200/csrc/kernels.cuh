@@ -223,6 +223,27 @@ __global__ void cast_f32_kernel(const float* __restrict__ src, void* __restrict_
     store_from_f32(dst, i, src[i], prec);
 }
 
+// bf16 -> fp32 (the all-reduced bf16 gradient bucket back into the flat fp32
+// buffer the optimizer reads); 8 elements per thread-iteration.
+__global__ void widen_bf16_kernel(const __nv_bfloat16* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  griddep_wait();
+  const int64_t n8 = n >> 3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = reinterpret_cast<const uint4*>(src)[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+    float4 a, b;
+    float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]), f2 = __bfloat1622float2(h[2]),
+           f3 = __bfloat1622float2(h[3]);
+    a = make_float4(f0.x, f0.y, f1.x, f1.y);
+    b = make_float4(f2.x, f2.y, f3.x, f3.y);
+    reinterpret_cast<float4*>(dst)[2 * i] = a;
+    reinterpret_cast<float4*>(dst)[2 * i + 1] = b;
+  }
+  for (int64_t i = (n8 << 3) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
 // Q (2f x 2r) fp32 -> compute precision, keeping only the diagonal blocks
 // [0,f)x[0,r) and [f,2f)x[r,2r) (the gate-gate and up-up products).
 __global__ void cast_blockdiag_kernel(const float* __restrict__ src, void* __restrict__ dst, int rows_half,

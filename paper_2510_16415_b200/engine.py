@@ -47,7 +47,8 @@ class StepEngine:
     def __init__(self, cfg: mdl.ModelConfig, precision: str = "bf16", seqs_per_microbatch: int = 32, r: int = 128,
                  tau: int = 100, optim_cfg: op.OptimConfig | None = None, seed: int = 0,
                  weights: mdl.ModelWeights | None = None, svd: SvdConfig | None = None, svd_budgeted: bool = False,
-                 group=None, fuse_lean: bool = True, max_group: int = 2, defer_layers: int | None = 4):
+                 group=None, fuse_lean: bool = True, max_group: int = 2, defer_layers: int | None = 4,
+                 grad_comm: str = "fp32", overlap_comm: bool = True):
         runtime.require_cuda()
         self.cfg = cfg
         self.precision = precision
@@ -94,6 +95,18 @@ class StepEngine:
         self.defer_layers = L if defer_layers is None else max(1, min(int(defer_layers), L))
         self._dyc = {}
         self._saved = {}
+        # Eq. (1) exchange (cluster.py:292-322): the pre-weighted flat gradient
+        # is all-reduced in buckets, in backward order (head, layer groups of
+        # `defer_layers` from the top, embedding), each on a communication
+        # stream as soon as its gradients are final — overlapped with the rest
+        # of the backward. grad_comm "bf16" casts each bucket to bf16 for the
+        # wire (and back to fp32 for the optimizer); "fp32" reduces in place.
+        if grad_comm not in ("fp32", "bf16"):
+            raise ContractViolation(f"grad_comm must be fp32 or bf16, got {grad_comm!r}")
+        self.grad_comm = grad_comm
+        self.overlap_comm = overlap_comm
+        self._comm = torch.cuda.Stream(device=self.device) if group is not None else None
+        self._gbf16 = None
         self._ws_lr = None
         self.xf = torch.empty(b, m, dtype=self.dtype, device=self.device)
         self.inv_f = torch.empty(b, **f32)
@@ -180,6 +193,38 @@ class StepEngine:
             self._saved[slot] = (mk(m), mk(f), mk(2 * f))
         return self._saved[slot]
 
+    def _layers_range(self, lo: int, hi: int) -> tuple:
+        """Flat-buffer element range holding every parameter of layers lo..hi."""
+        first = self.weights.offsets[f"layers.{lo}.q"]
+        name = f"layers.{hi}.norm_ffn"
+        return first, self.weights.offsets[name] + int(np.prod(self.weights.shapes[name]))
+
+    def _exchange(self, start: int, end: int) -> None:
+        """All-reduce(sum) of flat gradient elements [start, end) on the
+        communication stream, ordered after everything enqueued so far on the
+        compute stream (graph-capturable fork)."""
+        if self.group is None or end <= start:
+            return
+        import torch.distributed as dist
+
+        main = torch.cuda.current_stream()
+        if not self.overlap_comm:
+            dist.all_reduce(self.grad[start:end], op=dist.ReduceOp.SUM, group=self.group)
+            return
+        self._comm.wait_stream(main)
+        with torch.cuda.stream(self._comm):
+            g = self.grad[start:end]
+            if self.grad_comm == "bf16":
+                if self._gbf16 is None:
+                    self._gbf16 = torch.empty(self.weights.total, dtype=torch.bfloat16, device=self.device)
+                cs = self._comm.cuda_stream
+                bb = self._gbf16[start:end]
+                _lib.call("mecefo_cast_bf16", g.data_ptr(), bb.data_ptr(), end - start, cs)
+                dist.all_reduce(bb, op=dist.ReduceOp.SUM, group=self.group)
+                _lib.call("mecefo_widen_bf16", bb.data_ptr(), g.data_ptr(), end - start, cs)
+            else:
+                dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+
     def _flush_lowrank(self, jobs: list, b: int, s: int) -> None:
         """The deferred low-rank FFN Wgrads of a group of lean layers, as
         grouped launches (mecefo_lowrank_wgrads_batched)."""
@@ -253,12 +298,14 @@ class StepEngine:
                 pc.svd_calls += len(lead.basis)
         return lead.packed(self.precision, down_rows=mdl.ffn_storage(self.cfg))
 
-    def microbatch(self, mb: Microbatch, loss_ptr: int) -> None:
-        self._run([mb], loss_ptr)
+    def microbatch(self, mb: Microbatch, loss_ptr: int, comm: bool = False) -> None:
+        self._run([mb], loss_ptr, comm)
 
-    def _run(self, mbs: list, loss_ptr: int) -> None:
+    def _run(self, mbs: list, loss_ptr: int, comm: bool = False) -> None:
         """Forward + backward of len(mbs) microbatches stacked into one pass;
-        loss_ptr receives len(mbs) consecutive per-microbatch mean losses."""
+        loss_ptr receives len(mbs) consecutive per-microbatch mean losses.
+        comm: this is the GPU's last pass of the iteration, so each gradient
+        bucket is final once this pass has produced it: exchange it."""
         cfg, eng, s = self.cfg, self.eng, runtime.stream_ptr()
         n, b1 = len(mbs), self.b
         b = n * b1
@@ -293,8 +340,11 @@ class StepEngine:
                   w.shadow_view("unembedding").data_ptr(), self.dx[cur].data_ptr(),
                   runtime.ptr(dxc(cfg.layers) if defer else self.dx_c[cur]),
                   self._gp("final_norm"), self._gp("unembedding"), mb.alpha_global, b, ws, wn, s)
+        if comm:  # head bucket: final_norm + unembedding (the flat buffer's tail)
+            self._exchange(self.weights.offsets["final_norm"], self.weights.total)
         jobs, keeps = [], []
         since_flush = 0
+        pending_hi = cfg.layers - 1
         for l in reversed(range(cfg.layers)):
             nxt = 1 - cur
             dyc_in = dxc(l + 1) if defer else self.dx_c[cur]
@@ -326,14 +376,23 @@ class StepEngine:
                           self.dx[nxt].data_ptr(), runtime.ptr(dxc_out), ctypes.byref(g), b, ws, wn, s)
             cur = nxt
             since_flush += 1
-            if defer and since_flush == self.defer_layers:  # rotating buffers are about to be reused
-                self._flush_lowrank(jobs, b, s)
+            if since_flush == self.defer_layers:  # rotating buffers are about to be reused
+                if defer:
+                    self._flush_lowrank(jobs, b, s)
+                if comm:  # layers l .. pending_hi are final
+                    self._exchange(*self._layers_range(l, pending_hi))
+                    pending_hi = l - 1
                 since_flush = 0
         if defer:
             self._flush_lowrank(jobs, b, s)
+        if comm and pending_hi >= 0:
+            self._exchange(*self._layers_range(0, pending_hi))
         self._keep = keeps
         _lib.call("mecefo_embedding_backward", eng.handle, self.tok.data_ptr(), self.dx[cur].data_ptr(),
                   self._gp("embedding"), mb.alpha_global, b, s)
+        if comm:
+            e0 = self.weights.offsets["embedding"]
+            self._exchange(e0, e0 + int(np.prod(self.weights.shapes["embedding"])))
 
     # ------------------------------------------------------------ optimizer
     def _seg_slot(self, slot: int, nseg: int):
@@ -423,22 +482,30 @@ class StepEngine:
         self._prerefresh(mbs)
         self._memset0(self.grad)
         self._memset0(losses)
+        comm = self.group is not None
         if self._fusable(mbs):
             ranks = [mb.rank for mb in mbs]
             if ranks == list(range(ranks[0], ranks[0] + len(ranks))):
-                self._run(mbs, losses.data_ptr() + 4 * ranks[0])  # per-rank losses land in place
+                self._run(mbs, losses.data_ptr() + 4 * ranks[0], comm)  # per-rank losses land in place
             else:
-                self._run(mbs, self._loss_tmp.data_ptr())
+                self._run(mbs, self._loss_tmp.data_ptr(), comm)
                 for i, j in enumerate(ranks):  # device-to-device, graph-capturable
                     losses[j:j + 1].copy_(self._loss_tmp[i:i + 1])
         else:
-            for mb in mbs:
-                self.microbatch(mb, losses.data_ptr() + 4 * mb.rank)
+            for k, mb in enumerate(mbs):
+                self.microbatch(mb, losses.data_ptr() + 4 * mb.rank, comm and k == len(mbs) - 1)
+        if comm and not mbs:  # a GPU with no microbatch (its rank failed) still joins every bucket
+            self._exchange(self.weights.offsets["final_norm"], self.weights.total)
+            for hi in range(self.cfg.layers - 1, -1, -self.defer_layers):
+                self._exchange(*self._layers_range(max(0, hi - self.defer_layers + 1), hi))
+            e0 = self.weights.offsets["embedding"]
+            self._exchange(e0, e0 + int(np.prod(self.weights.shapes["embedding"])))
         self.iter += 1
-        if self.group is not None:
+        if comm:
             import torch.distributed as dist
 
-            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
+            if self.overlap_comm:
+                torch.cuda.current_stream().wait_stream(self._comm)  # join before the optimizer
             dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=self.group)
 
     def step(self, mbs: list, n_ranks: int, lr: float, skip=(), check: bool = True) -> torch.Tensor:
