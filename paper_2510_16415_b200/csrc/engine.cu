@@ -674,9 +674,13 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
     CUtensorMap tq, tdo;
     TRY(make_tmap(e, &tq, a.qkv, 3 * a.m, tokens, a.ld_qkv, 64, 64));
     TRY(make_tmap(e, &tdo, a.dctx, a.m, tokens, a.ld_ctx, 64, 64));
-    AttnBwdTcArgs t{a.ctx, a.dctx, a.lse, a.dqkv, a.cosT, a.sinT, a.T, a.H, a.m, a.rope, a.scale};
+    // theta table: stored after the seq_len x (hd/2) cos table (as for the QKV epilogue)
+    AttnBwdTcArgs t{a.ctx, a.dctx, a.lse, a.dqkv, e->rope_cos + (size_t)e->d.seq_len * (hd / 2), a.T, a.H, a.m,
+                    a.rope, a.scale};
     TRY(ensure_smem((const void*)attn_bwd_tc_kernel, ABT_SMEM));
-    CUDA_TRY(pdl_launch(attn_bwd_tc_kernel, dim3((unsigned)((tokens / a.T) * a.H)), dim3(ABT_THREADS), ABT_SMEM, s, tq, tdo, t));
+    const int items = (int)((tokens / a.T) * a.H);
+    CUDA_TRY(pdl_launch(attn_bwd_tc_kernel, dim3((unsigned)std::min(items, kNumSMs)), dim3(ABT_THREADS), ABT_SMEM, s,
+                        tq, tdo, t, items));
     return check_launch("attn_bwd_tc_kernel");
   }
   ProfScope prof(backward ? "attn_bwd" : "attn_fwd", (backward ? 4.0 : 2.0) * tokens * a.T * a.m,

@@ -456,7 +456,12 @@ class StepEngine:
                 mats.append(w)
                 ranks.append(min(self.r, w.shape[1]))
                 owners.append((l, kind))
+        import time
+
+        t0 = time.perf_counter()
         bases = self._solve_bases(mats, ranks)
+        torch.cuda.current_stream().synchronize()  # the solve reads its convergence flags on the host anyway
+        self.last_refresh_s = time.perf_counter() - t0
         for (l, kind), v1 in zip(owners, bases):
             for pc in due[l]:
                 pc.set_basis(kind, v1)
