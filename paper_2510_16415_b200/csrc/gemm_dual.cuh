@@ -101,6 +101,30 @@ __device__ __forceinline__ void stage_store32_lsu(uint8_t* box, const float* v, 
   __syncwarp();
 }
 
+// 32 fp32 -> 16 bf16x2 words (the packed form an epilogue keeps while it
+// loads its next chunk).
+__device__ __forceinline__ void pack32_bf16(const float* v, uint32_t* w) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    w[j] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+// stage_store32_db for an already packed bf16 32-column row segment.
+__device__ __forceinline__ void stage_store32_db_packed(uint8_t* stg, int& sb, const CUtensorMap* map,
+                                                        const uint32_t* w, int c0, int r0, int lane) {
+  uint8_t* box = stg + sb * 2048;
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+  uint8_t* row = box + lane * 64;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    *reinterpret_cast<uint4*>(row + ((u ^ ((lane >> 1) & 3)) << 4)) =
+        make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+  stage_commit(box, map, 0, c0, r0, lane);
+  sb ^= 1;
+}
+
 constexpr int D2_NP = 128;
 constexpr int D2_STAGE_BYTES = TC_BM * TC_BK * 2 + 2 * D2_NP * TC_BK * 2;  // 16 KB A + 32 KB B (max of the phases)
 constexpr int D2_STAGES = 4;
@@ -471,6 +495,58 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
       tc_fence_after();
       const int r0 = mt * 2 * TC_BM + (int)crank * TC_BM + quad * 32;
       const uint32_t lanes = tmem_base + ((uint32_t)(quad * 32) << 16);
+      if constexpr (CPW == 2) {
+        // Early release: chunk 0 is loaded, computed and kept PACKED (48
+        // words) while chunk 1 is loaded; the tile's TMEM is released right
+        // after that second load — before any store — so the next tile's
+        // gate|up product waits for two TMEM reads and one SwiGLU pass
+        // instead of a whole chunk's three staged stores as well.
+        uint32_t pa[16], pg[16], pu[16];
+        const int c0 = cbase, n00 = nt * D2_NP + c0 * 32;
+        const bool ok0 = n00 < p.NP && r0 < p.M;
+        {
+          const uint32_t gcol = (uint32_t)((c0 >> 1) * 128 + (c0 & 1) * 32), ucol = gcol + 64u;
+          float d[32], g[32], u[32];
+          tmem_ld16_nowait(lanes + dcol + c0 * 32, d);
+          tmem_ld16_nowait(lanes + dcol + c0 * 32 + 16, d + 16);
+          tmem_ld16_nowait(lanes + gcol, g);
+          tmem_ld16_nowait(lanes + gcol + 16, g + 16);
+          tmem_ld16_nowait(lanes + ucol, u);
+          tmem_ld16_nowait(lanes + ucol + 16, u + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) swiglu_bwd_elem(g[j], u[j], d[j]);
+          pack32_bf16(d, pa);
+          pack32_bf16(g, pg);
+          pack32_bf16(u, pu);
+        }
+        const int c1 = cbase + 1, n01 = nt * D2_NP + c1 * 32;
+        const uint32_t gcol = (uint32_t)((c1 >> 1) * 128 + (c1 & 1) * 32), ucol = gcol + 64u;
+        float d[32], g[32], u[32];
+        tmem_ld16_nowait(lanes + dcol + c1 * 32, d);
+        tmem_ld16_nowait(lanes + dcol + c1 * 32 + 16, d + 16);
+        tmem_ld16_nowait(lanes + gcol, g);
+        tmem_ld16_nowait(lanes + gcol + 16, g + 16);
+        tmem_ld16_nowait(lanes + ucol, u);
+        tmem_ld16_nowait(lanes + ucol + 16, u + 16);
+        tmem_wait_ld();
+        tc_fence_before();  // this warp's TMEM reads of the tile are done: release to the leader's MMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(edone, 0);
+        if (ok0) {
+          if (p.has_act) stage_store32_db_packed(stg, sb, &tmAct, pa, n00, r0, lane);
+          stage_store32_db_packed(stg, sb, &tmDg, pg, n00, r0, lane);
+          stage_store32_db_packed(stg, sb, &tmDu, pu, n00, r0, lane);
+        }
+        if (n01 < p.NP && r0 < p.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) swiglu_bwd_elem(g[j], u[j], d[j]);
+          if (p.has_act) stage_store32_db(stg, sb, &tmAct, d, n01, r0, lane);
+          stage_store32_db(stg, sb, &tmDg, g, n01, r0, lane);
+          stage_store32_db(stg, sb, &tmDu, u, n01, r0, lane);
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int cc = 0; cc < CPW; ++cc) {
         const int c = cbase + cc;
