@@ -294,6 +294,10 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   p.tiles_m_cl = (p.tiles_m + CL - 1) / CL;
   p.split_tiles = p.tiles_m_cl * p.tiles_n * p.split;
   p.num_tiles_cl = p.split_tiles * ng;
+  // A-heavy GEMMs with few N tiles (d_h2, the residual GEMMs, head d_xf): N-fastest
+  // order so an A row block is streamed from HBM once (measured: d_h2 read
+  // 159 MB for a 90 MB A with the M-fastest order)
+  p.n_fast = (p.tiles_n >= 2 && p.tiles_n <= 8 && (double)g.M >= 4.0 * (double)g.N * (g.paired ? 2 : 1)) ? 1 : 0;
   p.epi = g.epi;
   // output slots -> TMA store / reduce-add maps (32 x 32 boxes, swizzled)
   TcOut outs{};
@@ -396,6 +400,13 @@ bool use_cluster(const GemmCall& g, int BN) {
 // intensity: 128x256 tiles read 85 flop/B, 128x64 only 51).
 int choose_bn(const GemmCall& g) {
   if (g.force_bn) return g.force_bn;
+#ifdef MECEFO_TIMING_KNOBS
+  // timing experiments only: MECEFO_BN_FOR="tag=BN,tag=BN"
+  if (const char* v = getenv("MECEFO_BN_FOR")) {
+    const char* hit = g.tag ? strstr(v, g.tag) : nullptr;
+    if (hit && hit[strlen(g.tag)] == '=') return atoi(hit + strlen(g.tag) + 1);
+  }
+#endif
   const int64_t nacc = g.paired ? 2 * g.N : g.N;
   const int64_t tm = (g.M + 127) / 128;
   // per-flop penalty of narrower tiles (L2-bound operand traffic), measured

@@ -65,6 +65,7 @@ struct GemmDev {
   int tiles_m, tiles_n, num_tiles;
   int tiles_m_cl, num_tiles_cl;  // tiles in units of CTA clusters along M (CL = 1 or 2); x groups
   int split_tiles;               // tiles_m_cl * tiles_n * split (one group)
+  int n_fast;                    // tile order: N fastest (A-heavy GEMMs: the N tiles of an A row block run together)
   Epilogue epi;
 };
 
@@ -244,10 +245,18 @@ __device__ __forceinline__ void decode_tile_cl(const GemmDev& p, int t, int cran
                                                int& ks, int& grp) {
   grp = t / p.split_tiles;
   t -= grp * p.split_tiles;
-  const int mp = t % p.tiles_m_cl;
-  int rest = t / p.tiles_m_cl;
-  nt = rest % p.tiles_n;
-  ks = rest / p.tiles_n;
+  int mp;
+  if (p.n_fast) {  // consecutive tiles share one A row block (read from HBM once, L2 hits for the rest)
+    nt = t % p.tiles_n;
+    const int rest = t / p.tiles_n;
+    mp = rest % p.tiles_m_cl;
+    ks = rest / p.tiles_m_cl;
+  } else {         // consecutive tiles share one B tile
+    mp = t % p.tiles_m_cl;
+    const int rest = t / p.tiles_m_cl;
+    nt = rest % p.tiles_n;
+    ks = rest / p.tiles_n;
+  }
   mt = mp * cl + crank;
 }
 

@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
         tc_fence_before();  // this warp's TMEM reads of the tile are done: release to the leader's MMA
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(edone, 0);
-        if (ok0) {
+        if (ok0 && !(p.dbg & 1)) {  // (dbg: timing experiments only)
           if (p.has_act) stage_store32_db_packed(stg, sb, &tmAct, pa, n00, r0, lane);
           stage_store32_db_packed(stg, sb, &tmDg, pg, n00, r0, lane);
           stage_store32_db_packed(stg, sb, &tmDu, pu, n00, r0, lane);
@@ -541,6 +541,13 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
         if (n01 < p.NP && r0 < p.M) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) swiglu_bwd_elem(g[j], u[j], d[j]);
+          if (p.dbg & 1) {  // timing experiments only: keep the math, drop the stores
+            float sink = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sink += d[j] + g[j] + u[j];
+            if (sink == 12345.f) p.act[0] = __float2bfloat16_rn(sink);
+            continue;
+          }
           if (p.has_act) stage_store32_db(stg, sb, &tmAct, d, n01, r0, lane);
           stage_store32_db(stg, sb, &tmDg, g, n01, r0, lane);
           stage_store32_db(stg, sb, &tmDu, u, n01, r0, lane);
