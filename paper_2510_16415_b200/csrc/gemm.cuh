@@ -390,7 +390,7 @@ struct TcCfg {
   static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int EPI_BYTES = TC_EPI_WARPS * TC_STAGE_OUT;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 // Output slot s of an epilogue: 0 = `out`, 1 = `out2`, 2 = `out2 + off2`.
@@ -596,7 +596,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_holder + 2);  // per-epilogue-warp residual-box barriers
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_holder + 2);  // per-epilogue-warp residual-box barriers (x2)
+  // fp32 residual epilogues (x + f(x)) with BN >= 128 run the operand ring one
+  // stage short and give each epilogue warp a second residual box in the
+  // freed stage, so the residual of a chunk is TMA-prefetched while the
+  // previous chunk (or the tile's mainloop) is in flight
+  const bool res_pf = BN >= 128 && NG == 1 && p.epi.kind == EPI_STORE && p.epi.residual != nullptr &&
+                      outs.used[0] && outs.prec[0] == PREC_F32 && !p.paired && !outs.used[1] && !outs.used[2] &&
+                      p.kb_per_split <= 12;  // short K only: a long mainloop needs the full ring (measured:
+                                             // o_residual K=512 33 -> 29 us, down_residual K=1376 37 -> 39 us)
+  const int nst = res_pf ? C::STAGES - 1 : C::STAGES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 32 * TC_EPI_WARPS);
     }
-    for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
+    for (int w = 0; w < 2 * TC_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.a[0])) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.b[0])) : "memory");
@@ -685,7 +694,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tma_load_2d(b + c * 8192, tmB, &full[stage], col, k0);
             }
           }
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -722,7 +731,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc_commit_mc(&empty[stage], kMask);  // the stage holds the peer's multicast half too
           else
             tc_commit(&empty[stage]);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -742,6 +751,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool res_tma = p.epi.kind == EPI_STORE && p.epi.residual != nullptr && outs.used[0] &&
                          outs.prec[0] == PREC_F32 && !p.paired;
     uint32_t rphase = 0;
+    uint32_t pf_phase[2] = {0u, 0u};
+    // res_pf: this warp's two residual boxes (the staging box and one in the
+    // spare operand stage) and their barriers rbar[ew], rbar[8 + ew]
+    uint8_t* pf_box[2] = {stg, ew < 4 ? sA + (C::STAGES - 1) * C::A_BYTES + ew * TC_STAGE_OUT
+                                      : sB + (C::STAGES - 1) * C::B_BYTES + (ew - 4) * TC_STAGE_OUT};
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int NCHUNK_PLAIN = BN / 32;
@@ -750,15 +764,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int mt, nt, ks, grp;
       decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
       const CUtensorMap* tmO0 = &mp.o0[NG > 1 ? grp : 0];
+      const int r0 = mt * TC_BM + quad * 32;
+      const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
+      const int cbase = p.paired ? nt * (BN / 2) : nt * BN;
+      if (res_pf) {  // this tile's first two residual boxes, before its accumulator is even ready
+        stage_wait(lane);  // every earlier store has read its box
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int cj = half + 2 * j;
+            if (cj < nchunks && cbase + cj * 32 < p.N) {
+              mbar_expect_tx(&rbar[8 * j + ew], 32 * 32 * 4);
+              tma_load_2d(pf_box[j], &mp.r, &rbar[8 * j + ew], cbase + cj * 32, r0);
+            }
+          }
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int r0 = mt * TC_BM + quad * 32;
       const int row = r0 + lane;
       const bool row_ok = row < p.M;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
-      const int cbase = p.paired ? nt * (BN / 2) : nt * BN;
       bool released = false;
+      int pf_i = 0;  // this warp's chunk index within the tile
       // hd = 64 RoPE: every chunk this warp handles (c = half + 2k, 32 columns)
       // uses the same 16 frequencies j = 16*half + i, so the row's (cos, sin)
       // are computed once per tile instead of once per head
@@ -778,10 +806,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
 #pragma unroll 1
-      for (int c = half; c < nchunks; c += 2) {
+      for (int c = half; c < nchunks; c += 2, ++pf_i) {
         const int n0 = cbase + c * 32;
         if (n0 >= p.N) continue;  // warp-uniform
-        if (res_tma) {
+        uint8_t* rbox = res_pf ? pf_box[pf_i & 1] : stg;
+        if (res_tma && !res_pf) {
           stage_wait(lane);  // the previous store has read the box
           if (lane == 0) {
             mbar_expect_tx(&rbar[ew], 32 * 32 * 4);
@@ -808,7 +837,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int slot = 0; slot < 3; ++slot) {  // unrolled: outs.* indexed statically (no local-memory copy)
           if (!outs.used[slot]) continue;
           const bool rs = slot == 0 && res_tma;
-          if (rs) {
+          uint8_t* box = rs ? rbox : stg;
+          if (rs && res_pf) {
+            mbar_wait(&rbar[8 * (pf_i & 1) + ew], pf_phase[pf_i & 1]);
+            pf_phase[pf_i & 1] ^= 1u;
+          } else if (rs) {
             mbar_wait(&rbar[ew], rphase);
             rphase ^= 1;
           } else {
@@ -822,16 +855,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if constexpr (ROPE) rp = (rope_pre && n0h + 16 <= p.epi.rope_cols) ? rcs + hh * 8 : nullptr;
             epi_slot16(p.epi, slot, row, n0h, p.N - n0h, row_ok, g + hh * 16, u + hh * 16, o, rs, rp);
             if (rs) {  // + residual from the staging box (this lane's row, 16 columns)
-              const uint8_t* rrow = stg + lane * 128;
+              const uint8_t* rrow = box + lane * 128;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float4 r4 = *reinterpret_cast<const float4*>(rrow + (((hh * 4 + q) ^ (lane & 7)) << 4));
                 o[4 * q] += r4.x; o[4 * q + 1] += r4.y; o[4 * q + 2] += r4.z; o[4 * q + 3] += r4.w;
               }
             }
-            stage_write16(stg, o, outs.prec[slot], hh, lane);
+            stage_write16(box, o, outs.prec[slot], hh, lane);
           }
-          stage_commit(stg, slot == 0 ? tmO0 : (slot == 1 ? &mp.o1 : &mp.o2), outs.reduce[slot], n0, r0, lane);
+          stage_commit(box, slot == 0 ? tmO0 : (slot == 1 ? &mp.o1 : &mp.o2), outs.reduce[slot], n0, r0, lane);
+        }
+        if (res_pf) {  // refill this box with the residual of the warp's chunk after next
+          const int cn = c + 4;
+          if (cn < nchunks && cbase + cn * 32 < p.N) {
+            stage_wait(lane);  // the store just issued has read the box
+            if (lane == 0) {
+              mbar_expect_tx(&rbar[8 * (pf_i & 1) + ew], 32 * 32 * 4);
+              tma_load_2d(rbox, &mp.r, &rbar[8 * (pf_i & 1) + ew], cbase + cn * 32, r0);
+            }
+          }
         }
       }
       if (!released) {
