@@ -391,7 +391,11 @@ bool use_cluster(const GemmCall& g, int BN) {
   const int64_t cpt = g.paired ? BN / 2 : BN;
   const int64_t tiles = ((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt);
   // (paired gate|up GEMMs measured 9% slower clustered: excluded)
-  return BN >= 128 && !g.paired && (g.M + 127) / 128 >= 2 && tiles >= 1024;
+  int64_t min_tiles = 1024;
+#ifdef MECEFO_TIMING_KNOBS
+  if (const char* v = getenv("MECEFO_CLUSTER_MIN_TILES")) min_tiles = atoll(v);
+#endif
+  return BN >= 128 && !g.paired && (g.M + 127) / 128 >= 2 && tiles >= min_tiles;
 }
 
 // Tile width for the tcgen05 path. The MMA time of a tile is proportional to
