@@ -29,10 +29,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, R=4):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    R, L = 4, 3
+    L = 3
     # replicated control plane: same scenario, same seed on every process
     state = cl.ClusterState(cl.ClusterConfig(dp=1, pp=R, layers=R),
                             cl.FailureScenario(kind="per_iteration", probability=0.1, recovery_iterations=2, seed=11))
@@ -58,7 +58,7 @@ def _worker(rank, world, port, out_dir):
                     for k in cluster_ref.MHA:
                         g[f"layers.{l}.{k}"] = np.full(3, np.nan)  # poison: must never leak
             per_rank.append(g)
-        # this process executes the ranks routed to GPU == process rank (R=4 on 2 procs: j % 2)
+        # this process executes the ranks routed to GPU == process rank (R logical ranks on `world` procs: j % world)
         local = {n: torch.zeros(3, dtype=torch.float64) for n in names}
         for j in range(R):
             if route[j] % world != rank:
@@ -86,7 +86,7 @@ def _worker(rank, world, port, out_dir):
         results.append(it)
     gathered = [None] * world
     dist.all_gather_object(gathered, digests)
-    assert gathered[0] == gathered[1]
+    assert all(g == gathered[0] for g in gathered)
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump({"iterations": results, "digests": digests}, f)
     dist.destroy_process_group()
@@ -98,3 +98,11 @@ def test_two_process_plan_agreement_and_eq1_exchange(tmp_path):
     r0 = json.load(open(tmp_path / "rank0.json"))
     r1 = json.load(open(tmp_path / "rank1.json"))
     assert r0 == r1 and len(r0["iterations"]) >= 5
+
+
+def test_four_process_eight_rank_plan_agreement_and_eq1_exchange(tmp_path):
+    """The 8-rank ring (the 8-GPU layout's control plane) on 4 processes."""
+    world = 4
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), 8), nprocs=world, join=True)
+    docs = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(world)]
+    assert all(d == docs[0] for d in docs) and len(docs[0]["iterations"]) >= 5
