@@ -439,6 +439,7 @@ def run_scenario(args, dims, world, rank, local, group):
     import torch
 
     from paper_2510_16415_b200 import cluster as cl
+    from paper_2510_16415_b200.errors import UnrecoverableRankError
 
     job = Job(args, dims, world, rank, local, group)
     R, L = job.R, job.cfg.layers
@@ -481,6 +482,7 @@ def run_scenario(args, dims, world, rank, local, group):
 
     degraded_iters, refreshes, captures, events_log = 0, 0, 0, []
     kinds, marks, refresh_log = [], [], []
+    aborted = None  # the reference aborts on an unrecoverable state (cli exit 4): measured up to there
     run_len, last_key = 0, None
     job.barrier()
     torch.cuda.synchronize()
@@ -501,7 +503,12 @@ def run_scenario(args, dims, world, rank, local, group):
             evs += cl.reassign_takeover(state, 0.0, it)
             cl.validate_state(state)
         else:
-            evs = cl.step_cluster(state, 0.0, it)
+            try:
+                evs = cl.step_cluster(state, 0.0, it)
+            except UnrecoverableRankError as exc:  # every process sees it at the same iteration
+                aborted = {"iteration": it, "error": str(exc)}
+                marks.pop()
+                break
         for ev in evs:
             if ev["kind"] == "adopt":  # harness.py:384-388: the adopted rank's layers start fresh bases
                 j = ev["details"]["stage"]
@@ -538,7 +545,8 @@ def run_scenario(args, dims, world, rank, local, group):
     wall = time.perf_counter() - t0
     ms = job.max_over_ranks(max(st.elapsed_time(en), 1000 * wall))
     job.eng.check_status(sync=True)
-    tps = R * job.b * args.steps / (ms / 1000.0)
+    done = len(kinds)
+    tps = R * job.b * done / (ms / 1000.0) if done else 0.0
     breakdown = {}
     for k_, a_, b_ in zip(kinds, marks[:-1], marks[1:]):  # device time between iteration boundaries
         e_ = breakdown.setdefault(k_, [0, 0.0])
@@ -548,9 +556,9 @@ def run_scenario(args, dims, world, rank, local, group):
                  for k_, v in breakdown.items()}
     if rank == 0:
         out = {"metric": METRIC, "value": round(tps, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+               "warmup": args.warmup, "ms_per_step": round(ms / max(1, done), 3), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "impl": "ours",
-               "data": "synthetic (uniform tokens, PCG64)",
+               "data": "synthetic (uniform tokens, PCG64)", "iterations_completed": done, "aborted": aborted,
                "config": {"workload": workload(args.model, args.rank), "model": f"LLaMA-{args.model}",
                           "scenario": args.scenario, "logical_ranks": R, "microbatch_tokens": job.b,
                           "fail_prob": args.fail_prob if args.scenario == "c3" else None,
@@ -558,7 +566,7 @@ def run_scenario(args, dims, world, rank, local, group):
                           "refresh_period": TAU, "svd": "converged" if not args.budgeted_refresh else "budgeted"},
                "fault_free_tokens_per_s": round(ff_tps, 1),
                "drop_pct_time_averaged": round(100.0 * (1.0 - tps / ff_tps), 2),
-               "degraded_iteration_fraction": round(degraded_iters / args.steps, 3),
+               "degraded_iteration_fraction": round(degraded_iters / max(1, done), 3),
                "eager_refresh_iterations": refreshes, "graph_captures": captures,
                "graphs_cached": len(getattr(job.eng, "_graph_cache", {})),
                "precaptured_failure_plans": precaptured,
