@@ -456,42 +456,100 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_vec_kernel(const float* __res
   }
   const int r0 = blockIdx.x * rows_per_block;
   const int r1 = min(r0 + rows_per_block, rows);
-  for (int row = r0 + wid; row < r1; row += 8) {
-    const float* xr = x + (int64_t)row * m;
-    const float* dr = d + (int64_t)row * m;
-    const float iv = inv[row];
-    float4 xv[NV], dv[NV];
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int c = (i * 32 + lane) * 4;
-      if (c < m) {
-        xv[i] = *reinterpret_cast<const float4*>(xr + c);
-        dv[i] = *reinterpret_cast<const float4*>(dr + c);
-      } else {
-        xv[i] = dv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if constexpr (NV <= 4) {  // (wider rows would spill with two rows in registers)
+    // software pipeline over this warp's rows: the next row's x, d, residual
+    // and inv are in flight while the current row is reduced and written (one
+    // exposed memory latency per warp instead of two per row)
+    float4 xv[NV], dv[NV], rv[NV];
+    float iv = 0.f;
+    auto fetch = [&](int row, float4* xa, float4* da, float4* ra, float& ivr) {
+      const float* xr = x + (int64_t)row * m;
+      const float* dr = d + (int64_t)row * m;
+      ivr = inv[row];
+  #pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = (i * 32 + lane) * 4;
+        const bool ok = c < m;
+        xa[i] = ok ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        da[i] = ok ? *reinterpret_cast<const float4*>(dr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ra[i] = (ok && resid) ? *reinterpret_cast<const float4*>(resid + (int64_t)row * m + c)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      s += dv[i].x * gs[i].x * xv[i].x + dv[i].y * gs[i].y * xv[i].y + dv[i].z * gs[i].z * xv[i].z +
-           dv[i].w * gs[i].w * xv[i].w;
-      acc[i].x += dv[i].x * xv[i].x * iv;
-      acc[i].y += dv[i].y * xv[i].y * iv;
-      acc[i].z += dv[i].z * xv[i].z * iv;
-      acc[i].w += dv[i].w * xv[i].w * iv;
-    }
-    s = warp_sum(s) / (float)m;
-    const float k = iv * iv * iv * s;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int c = (i * 32 + lane) * 4;
-      if (c < m) {
-        float4 o = make_float4(dv[i].x * gs[i].x * iv - xv[i].x * k, dv[i].y * gs[i].y * iv - xv[i].y * k,
-                               dv[i].z * gs[i].z * iv - xv[i].z * k, dv[i].w * gs[i].w * iv - xv[i].w * k);
-        if (resid) {
-          const float4 rr = *reinterpret_cast<const float4*>(resid + (int64_t)row * m + c);
-          o.x += rr.x; o.y += rr.y; o.z += rr.z; o.w += rr.w;
+    };
+    if (r0 + wid < r1) fetch(r0 + wid, xv, dv, rv, iv);
+    for (int row = r0 + wid; row < r1; row += 8) {
+      float4 xn[NV], dn[NV], rn[NV];
+      float ivn = 0.f;
+      if (row + 8 < r1) fetch(row + 8, xn, dn, rn, ivn);
+      float s = 0.f;
+  #pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        s += dv[i].x * gs[i].x * xv[i].x + dv[i].y * gs[i].y * xv[i].y + dv[i].z * gs[i].z * xv[i].z +
+             dv[i].w * gs[i].w * xv[i].w;
+        acc[i].x += dv[i].x * xv[i].x * iv;
+        acc[i].y += dv[i].y * xv[i].y * iv;
+        acc[i].z += dv[i].z * xv[i].z * iv;
+        acc[i].w += dv[i].w * xv[i].w * iv;
+      }
+      s = warp_sum(s) / (float)m;
+      const float k = iv * iv * iv * s;
+  #pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = (i * 32 + lane) * 4;
+        if (c < m) {
+          float4 o = make_float4(dv[i].x * gs[i].x * iv - xv[i].x * k, dv[i].y * gs[i].y * iv - xv[i].y * k,
+                                 dv[i].z * gs[i].z * iv - xv[i].z * k, dv[i].w * gs[i].w * iv - xv[i].w * k);
+          o.x += rv[i].x; o.y += rv[i].y; o.z += rv[i].z; o.w += rv[i].w;  // zeros without a residual
+          *reinterpret_cast<float4*>(dx + (int64_t)row * m + c) = o;
+          if (dx_lp) store4(dx_lp, (int64_t)row * m + c, o, lp_prec);
         }
-        *reinterpret_cast<float4*>(dx + (int64_t)row * m + c) = o;
-        if (dx_lp) store4(dx_lp, (int64_t)row * m + c, o, lp_prec);
+      }
+  #pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        xv[i] = xn[i];
+        dv[i] = dn[i];
+        rv[i] = rn[i];
+      }
+      iv = ivn;
+    }
+  } else {
+    for (int row = r0 + wid; row < r1; row += 8) {
+      const float* xr = x + (int64_t)row * m;
+      const float* dr = d + (int64_t)row * m;
+      const float iv = inv[row];
+      float4 xv[NV], dv[NV];
+      float s = 0.f;
+  #pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = (i * 32 + lane) * 4;
+        if (c < m) {
+          xv[i] = *reinterpret_cast<const float4*>(xr + c);
+          dv[i] = *reinterpret_cast<const float4*>(dr + c);
+        } else {
+          xv[i] = dv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        s += dv[i].x * gs[i].x * xv[i].x + dv[i].y * gs[i].y * xv[i].y + dv[i].z * gs[i].z * xv[i].z +
+             dv[i].w * gs[i].w * xv[i].w;
+        acc[i].x += dv[i].x * xv[i].x * iv;
+        acc[i].y += dv[i].y * xv[i].y * iv;
+        acc[i].z += dv[i].z * xv[i].z * iv;
+        acc[i].w += dv[i].w * xv[i].w * iv;
+      }
+      s = warp_sum(s) / (float)m;
+      const float k = iv * iv * iv * s;
+  #pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = (i * 32 + lane) * 4;
+        if (c < m) {
+          float4 o = make_float4(dv[i].x * gs[i].x * iv - xv[i].x * k, dv[i].y * gs[i].y * iv - xv[i].y * k,
+                                 dv[i].z * gs[i].z * iv - xv[i].z * k, dv[i].w * gs[i].w * iv - xv[i].w * k);
+          if (resid) {
+            const float4 rr = *reinterpret_cast<const float4*>(resid + (int64_t)row * m + c);
+            o.x += rr.x; o.y += rr.y; o.z += rr.z; o.w += rr.w;
+          }
+          *reinterpret_cast<float4*>(dx + (int64_t)row * m + c) = o;
+          if (dx_lp) store4(dx_lp, (int64_t)row * m + c, o, lp_prec);
+        }
       }
     }
   }
