@@ -1,9 +1,12 @@
-"""Converged batched refresh on the bench model (C1 LLaMA-60M, 8 layers x
-gate/up/down, r=128, tol 1e-9): wall time and device time per kernel tag."""
-import ctypes, time, torch
+"""Converged batched refresh of every layer's gate/up/down (C1 LLaMA-60M by
+default; argv[1] in 60M/350M/1B), r=128, tol 1e-9: wall time and device
+time per kernel tag."""
+import ctypes, sys, time, torch
 from collections import defaultdict
 from paper_2510_16415_b200 import _lib, linalg, model as mdl
-cfg = mdl.ModelConfig(vocab=32000, hidden=512, heads=8, ffn_intermediate=1376, layers=8, seq_len=256)
+DIMS = {"60M": (512, 1376, 8, 8), "350M": (1024, 2736, 16, 24), "1B": (2048, 5461, 32, 24)}
+m_, f_, H_, L_ = DIMS[sys.argv[1] if len(sys.argv) > 1 else "60M"]
+cfg = mdl.ModelConfig(vocab=32000, hidden=m_, heads=H_, ffn_intermediate=f_, layers=L_, seq_len=256)
 w = mdl.init_weights(cfg, 0, precision="bf16")
 ws, ranks = [], []
 for lw in w.layers:
@@ -22,12 +25,13 @@ lib = _lib.load()
 lib.mecefo_profile_enable(1)
 linalg.refresh_bases(ws, ranks, svd); torch.cuda.synchronize()
 agg = defaultdict(lambda: [0.0, 0])
+fl_ = defaultdict(float)
 for i in range(lib.mecefo_profile_count()):
     tag, ms, fl, by = ctypes.c_char_p(), ctypes.c_float(), ctypes.c_double(), ctypes.c_double()
     lib.mecefo_profile_record(i, ctypes.byref(tag), ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by))
-    agg[tag.value.decode()][0] += ms.value; agg[tag.value.decode()][1] += 1
+    agg[tag.value.decode()][0] += ms.value; agg[tag.value.decode()][1] += 1; fl_[tag.value.decode()] += fl.value
 lib.mecefo_profile_enable(0)
 tot = sum(v[0] for v in agg.values())
 print(f"device total {tot:.2f} ms")
 for k, (ms, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
-    print(f"{k:24s} {ms:8.3f} ms  {n} launches")
+    print(f"{k:24s} {ms:8.3f} ms  {n} launches  {fl_[k] / (ms / 1e3) / 1e12 if ms else 0:.2f} TFLOP/s")
