@@ -694,6 +694,7 @@ int attention(mecefo_engine* e, bool backward, AttnDev a, int64_t tokens, cudaSt
                     a.rope, a.scale};
     TRY(ensure_smem((const void*)attn_bwd_tc_kernel, ABT_SMEM));
     const int items = (int)((tokens / a.T) * a.H);
+    if (items <= 0) return MECEFO_OK;
     CUDA_TRY(pdl_launch(attn_bwd_tc_kernel, dim3((unsigned)std::min(items, kNumSMs)), dim3(ABT_THREADS), ABT_SMEM, s,
                         tq, tdo, t, items));
     return check_launch("attn_bwd_tc_kernel");
