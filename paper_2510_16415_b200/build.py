@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libmecefo.so")
 SOURCES = ["engine.cu", "refresh.cu"]
 DEPS = ["common.cuh", "host.h", "gemm.cuh", "kernels.cuh", "attention.cuh", "attention_tc.cuh", "attention_bwd_tc.cuh",
-        "gemm_dual.cuh", "subspace.cuh", "ce.cuh", "refresh.cuh"]
+        "gemm_dual.cuh", "gemm_norm.cuh", "subspace.cuh", "ce.cuh", "refresh.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -23,6 +23,7 @@
 #include "attention_tc.cuh"
 #include "attention_bwd_tc.cuh"
 #include "gemm_dual.cuh"
+#include "gemm_norm.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "subspace.cuh"
@@ -884,6 +885,39 @@ size_t mecefo_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t ra
   return (size_t)(tokens * per_tok + fixed);
 }
 
+namespace {
+
+// x1 = x + A W^T and h = rmsnorm(x1) * g, inv (gemm_norm.cuh): the fused
+// O-projection + norm of one block forward when m = 512 and the pass fills a
+// wave of row blocks; returns false when it does not apply.
+bool resid_norm_applies(const mecefo_engine* e, int64_t b) {
+#ifdef MECEFO_TIMING_KNOBS
+  if (getenv("MECEFO_NO_RESID_NORM")) return false;
+#endif
+  return e->prec == PREC_BF16 && e->d.hidden == GN_N && (b + TC_BM - 1) / TC_BM >= 100;
+}
+
+int resid_norm_gemm(mecefo_engine* e, const void* a, int64_t K, const void* w, const float* x, float* x1, void* h,
+                    float* inv, const float* gain, int64_t b, cudaStream_t s) {
+  ProfScope prof("fwd.o_residual_norm", 2.0 * b * GN_N * K,
+                 2.0 * (b * K + GN_N * K) + 4.0 * 2 * b * GN_N + 2.0 * b * GN_N + 4.0 * b, s);
+  GnMaps mp;
+  TRY(make_tmap(e, &mp.a, a, K, b, K, 64, TC_BM));
+  TRY(make_tmap(e, &mp.b, w, K, GN_N, K, 64, 256));
+  TRY(make_tmap(e, &mp.r, x, GN_N, b, GN_N, 32, 32, 1, 128));
+  TRY(make_tmap(e, &mp.o, x1, GN_N, b, GN_N, 32, 32, 1, 128));
+  TRY(make_tmap(e, &mp.h, h, GN_N, b, GN_N, 32, 32, 0, 64));
+  GnDev p{};
+  p.M = (int)b; p.K = (int)K; p.kblocks = (int)((K + TC_BK - 1) / TC_BK);
+  p.eps = kRmsEps; p.gain = gain; p.inv = inv;
+  TRY(ensure_smem((const void*)gemm_resid_norm_kernel, GN_SMEM));
+  CUDA_TRY(pdl_launch(gemm_resid_norm_kernel, dim3((unsigned)((b + TC_BM - 1) / TC_BM)), dim3(TC_THREADS), GN_SMEM, s,
+                      mp, p));
+  return check_launch("gemm_resid_norm_kernel");
+}
+
+}  // namespace
+
 int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* c, float* y, void* y_c,
                          int64_t tokens, int32_t mode, void* wsp, size_t ws_bytes, void* stream) {
   (void)y_c;
@@ -924,14 +958,19 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   a.qkv = qkv; a.ld_qkv = 3 * m; a.ctx = ctx; a.ld_ctx = m; a.lse = lse;
   TRY(attention(e, false, a, b, s));
   // x1 = x + ctx Wo^T                                          (model.py:332, 406)
-  g = GemmCall();
-  g.M = b; g.N = m; g.K = m;
-  g.a = {ctx, m, true}; g.b = {lw->w_o_c, m, true};
-  g.epi = epi_store(c->x1, m, PREC_F32, 1.f, 0.f, c->x, m);
-  g.tag = "fwd.o_residual";
-  TRY(run_gemm(e, g, s));
-  // h2 = rmsnorm(x1) * g_ffn; act = silu(h2 Wg^T) * (h2 Wu^T)  (model.py:213-216)
-  TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
+  // h2 = rmsnorm(x1) * g_ffn                                   (model.py:213)
+  if (resid_norm_applies(e, b)) {
+    TRY(resid_norm_gemm(e, ctx, m, lw->w_o_c, c->x, c->x1, h2, inv2, lw->norm_ffn, b, s));
+  } else {
+    g = GemmCall();
+    g.M = b; g.N = m; g.K = m;
+    g.a = {ctx, m, true}; g.b = {lw->w_o_c, m, true};
+    g.epi = epi_store(c->x1, m, PREC_F32, 1.f, 0.f, c->x, m);
+    g.tag = "fwd.o_residual";
+    TRY(run_gemm(e, g, s));
+    TRY(rmsnorm_fwd(e, c->x1, lw->norm_ffn, h2, inv2, b, m, s));
+  }
+  // act = silu(h2 Wg^T) * (h2 Wu^T)                            (model.py:214-216)
   g = GemmCall();
   g.M = b; g.N = f; g.K = m;
   g.a = {h2, m, true}; g.b = {lw->w_gu_c, m, true};

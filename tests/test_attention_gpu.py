@@ -112,3 +112,22 @@ def test_lean_backward_llama_shapes(cuda, hidden, heads, ffn, r):
     assert R.rel_err(dx.cpu().numpy(), dx_ref.reshape(x.shape)) < BF16_TOL
     for k in g:
         assert R.rel_err(g[k].cpu().numpy(), g_ref[k]) < BF16_TOL, k
+
+
+def test_forward_block_fused_residual_norm_at_bench_size(cuda):
+    """16384 tokens at C1 dims (the fused doubled microbatch): the O projection
+    and the following RMSNorm run as ONE kernel (gemm_norm.cuh, one CTA per
+    128-row block owning all 512 columns). x1, h2, inv2 and the block output
+    against the float64 oracle; the lean forward gives the identical output."""
+    seqs = 64
+    cfg, d, W, x, dy = _setup(T=256, seqs=seqs, seed=3)
+    y_ref, c_ref = R.block_fwd(d, W, 0, x.reshape(seqs, 256, -1), lean=False)
+    w = mdl.init_weights(cfg, 3, precision="bf16")
+    xt = torch.tensor(x, dtype=torch.float32, device="cuda")
+    y, cache = mdl.forward_block(cfg, w.layers[0], xt, mdl.CACHE_FULL)
+    assert R.rel_err(cache.x1.cpu().numpy(), c_ref["x1"].reshape(x.shape)) < BF16_TOL
+    assert R.rel_err(cache.full["h2"].float().cpu().numpy(), c_ref["ffn"]["h2"].reshape(x.shape)) < BF16_TOL
+    assert R.rel_err(cache.full["inv2"].cpu().numpy(), c_ref["ffn"]["inv2"].reshape(-1)) < 1e-2
+    assert R.rel_err(y.cpu().numpy(), y_ref.reshape(x.shape)) < BF16_TOL
+    y2, _ = mdl.forward_block(cfg, w.layers[0], xt, mdl.CACHE_FFN_INPUT_ONLY)
+    assert torch.equal(y, y2)
