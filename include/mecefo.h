@@ -170,6 +170,21 @@ size_t mecefo_workspace_bytes(const mecefo_engine* e, int64_t tokens, int32_t ra
 int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* cache, float* y,
                          void* y_c, int64_t tokens, int32_t mode, void* ws, size_t ws_bytes, void* stream);
 
+/* forward_block of a chain of blocks (model.py:461-463 calls them in turn):
+ * as mecefo_forward_block, plus
+ *   flags & MECEFO_FWD_H1_READY: cache->h1 / cache->inv1 already hold this
+ *     block's rmsnorm(x) * norm_mha and 1/rms (written by the previous block
+ *     of the chain), so its own norm pass is skipped;
+ *   next_norm_gain != NULL: the block also writes the NEXT block's
+ *     h1 = rmsnorm(y) * next_norm_gain into next_h1 (compute precision) and
+ *     1/rms into next_inv1 — fused into the residual down-projection when
+ *     hidden = 512 (one kernel owns whole rows), a separate pass otherwise.
+ * Same results as calling mecefo_forward_block per block. */
+#define MECEFO_FWD_H1_READY 1
+int mecefo_forward_block_chained(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* cache,
+                                 float* y, int64_t tokens, int32_t mode, int32_t flags, const float* next_norm_gain,
+                                 void* next_h1, float* next_inv1, void* ws, size_t ws_bytes, void* stream);
+
 /* approx.py:99-134 backward_block_neighbor: skip the MHA backward, recompute
  * the FFN from x1, FFN Wgrads low-rank through `proj` (NULL = exact Wgrads,
  * the proj=None branch), dx = dy + dx1_ffn. dy_c: optional compute-precision

@@ -21,6 +21,7 @@ PREC_F32 = 0
 PREC_BF16 = 1
 CACHE_FULL = 0
 CACHE_FFN_INPUT_ONLY = 1
+FWD_H1_READY = 1  # mecefo_forward_block_chained flags
 STATUS_BAD_TOKEN = 1
 STATUS_BAD_TARGET = 2
 STATUS_NONFINITE_GRAD = 4
@@ -175,6 +176,11 @@ _SIGNATURES = {
         c_int,
         [c_void_p, POINTER(LayerWeights), POINTER(BlockCache), c_void_p, c_void_p, c_int64, c_int32, c_void_p,
          c_size_t, c_void_p],
+    ),
+    "mecefo_forward_block_chained": (
+        c_int,
+        [c_void_p, POINTER(LayerWeights), POINTER(BlockCache), c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_size_t, c_void_p],
     ),
     "mecefo_backward_block_neighbor": (
         c_int,

@@ -898,8 +898,8 @@ bool resid_norm_applies(const mecefo_engine* e, int64_t b) {
 }
 
 int resid_norm_gemm(mecefo_engine* e, const void* a, int64_t K, const void* w, const float* x, float* x1, void* h,
-                    float* inv, const float* gain, int64_t b, cudaStream_t s) {
-  ProfScope prof("fwd.o_residual_norm", 2.0 * b * GN_N * K,
+                    float* inv, const float* gain, int64_t b, cudaStream_t s, const char* tag = "fwd.o_residual_norm") {
+  ProfScope prof(tag, 2.0 * b * GN_N * K,
                  2.0 * (b * K + GN_N * K) + 4.0 * 2 * b * GN_N + 2.0 * b * GN_N + 4.0 * b, s);
   GnMaps mp;
   TRY(make_tmap(e, &mp.a, a, K, b, K, 64, TC_BM));
@@ -918,9 +918,33 @@ int resid_norm_gemm(mecefo_engine* e, const void* a, int64_t K, const void* w, c
 
 }  // namespace
 
+namespace {
+int forward_block_impl(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* c, float* y,
+                       int64_t tokens, int32_t mode, int32_t flags, const float* next_gain, void* next_h1,
+                       float* next_inv1, void* wsp, size_t ws_bytes, void* stream);
+}  // namespace
+
 int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* c, float* y, void* y_c,
                          int64_t tokens, int32_t mode, void* wsp, size_t ws_bytes, void* stream) {
   (void)y_c;
+  return forward_block_impl(e, lw, c, y, tokens, mode, 0, nullptr, nullptr, nullptr, wsp, ws_bytes, stream);
+}
+
+int mecefo_forward_block_chained(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* c, float* y,
+                                 int64_t tokens, int32_t mode, int32_t flags, const float* next_norm_gain,
+                                 void* next_h1, float* next_inv1, void* wsp, size_t ws_bytes, void* stream) {
+  if ((flags & MECEFO_FWD_H1_READY) && (!c->h1 || !c->inv1))
+    return set_err(MECEFO_ERR_CONTRACT, "MECEFO_FWD_H1_READY needs cache->h1 and cache->inv1");
+  if (next_norm_gain && (!next_h1 || !next_inv1))
+    return set_err(MECEFO_ERR_CONTRACT, "next_norm_gain needs next_h1 and next_inv1");
+  return forward_block_impl(e, lw, c, y, tokens, mode, flags, next_norm_gain, next_h1, next_inv1, wsp, ws_bytes,
+                            stream);
+}
+
+namespace {
+int forward_block_impl(mecefo_engine* e, const mecefo_layer_weights* lw, mecefo_block_cache* c, float* y,
+                       int64_t tokens, int32_t mode, int32_t flags, const float* next_gain, void* next_h1,
+                       float* next_inv1, void* wsp, size_t ws_bytes, void* stream) {
   TRY(check_tokens(e, tokens));
   if (mode != MECEFO_CACHE_FULL && mode != MECEFO_CACHE_FFN_INPUT_ONLY)
     return set_err(MECEFO_ERR_CONTRACT, "unknown cache mode %d", mode);
@@ -930,8 +954,9 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   Ws ws(wsp, ws_bytes);
   void *h1 = c->h1, *qkv = c->qkv, *ctx = c->ctx, *h2 = c->h2, *act = c->act;
   float *inv1 = c->inv1, *lse = c->lse, *inv2 = c->inv2;
-  if (!full || !h1) TRY(ws.take(b * m * e->ps, &h1));
-  if (!full || !inv1) TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv1)));
+  const bool h1_ready = (flags & MECEFO_FWD_H1_READY) != 0;  // the previous block's down kernel wrote them
+  if (!h1_ready && (!full || !h1)) TRY(ws.take(b * m * e->ps, &h1));
+  if (!h1_ready && (!full || !inv1)) TRY(ws.take(b * 4, reinterpret_cast<void**>(&inv1)));
   if (!full || !qkv) TRY(ws.take(b * 3 * m * e->ps, &qkv));
   if (!full || !ctx) TRY(ws.take(b * m * e->ps, &ctx));
   if (!full) lse = nullptr;
@@ -941,7 +966,7 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   if (!full || !act) TRY(ws.take(b * f * e->ps, &act));
 
   // h1 = rmsnorm(x) * g_mha; qkv = h1 [Wq;Wk;Wv]^T            (model.py:404, 320-322)
-  TRY(rmsnorm_fwd(e, c->x, lw->norm_mha, h1, inv1, b, m, s));
+  if (!h1_ready) TRY(rmsnorm_fwd(e, c->x, lw->norm_mha, h1, inv1, b, m, s));
   GemmCall g;
   g.M = b; g.N = 3 * m; g.K = m;
   g.a = {h1, m, true}; g.b = {lw->w_qkv_c, m, true};
@@ -982,14 +1007,22 @@ int mecefo_forward_block(mecefo_engine* e, const mecefo_layer_weights* lw, mecef
   g.tag = "fwd.gu_swiglu";
   TRY(run_gemm(e, g, s));
   // y = x1 + act Wd^T                                          (model.py:217, 408)
+  // [+ the next block's h1 = rmsnorm(y) * g_mha', inv1'        (model.py:404, 183-186)]
+  if (next_gain && resid_norm_applies(e, b) && f % 8 == 0) {
+    TRY(resid_norm_gemm(e, act, f, lw->w_down_c, c->x1, y, next_h1, next_inv1, next_gain, b, s,
+                        "fwd.down_residual_norm"));
+    return MECEFO_OK;
+  }
   g = GemmCall();
   g.M = b; g.N = m; g.K = f;
   g.a = {act, f, true}; g.b = {lw->w_down_c, f, true};
   g.epi = epi_store(y, m, PREC_F32, 1.f, 0.f, c->x1, m);
   g.tag = "fwd.down_residual";
   TRY(run_gemm(e, g, s));
+  if (next_gain) TRY(rmsnorm_fwd(e, y, next_gain, next_h1, next_inv1, b, m, s));
   return MECEFO_OK;
 }
+}  // namespace
 
 namespace {
 

@@ -235,6 +235,18 @@ class StepEngine:
         _lib.call("mecefo_lowrank_wgrads_batched", self.eng.handle, arr, len(jobs), b, wsl, wnl, s)
         jobs.clear()
 
+    def _h1_scratch(self, k: int, b: int):
+        """Compute-precision h1 (b x m) and fp32 inv1 (b) of a lean block in a
+        chain (two alternating pairs: a block reads one and writes the next
+        block's into the other)."""
+        if not hasattr(self, "_h1s"):
+            self._h1s = {}
+        key = (k, b)
+        if key not in self._h1s:
+            self._h1s[key] = (torch.empty(b, self.cfg.hidden, dtype=self.dtype, device=self.device),
+                              torch.empty(b, dtype=torch.float32, device=self.device))
+        return self._h1s[key]
+
     def _lowrank_ws(self, b: int, count: int):
         n = int(_lib.load().mecefo_lowrank_batched_workspace_bytes(self.eng.handle, b, self.rp, count))
         if self._ws_lr is None or self._ws_lr.numel() < n:
@@ -320,15 +332,29 @@ class StepEngine:
         _lib.call("mecefo_embedding_forward", eng.handle, self.tok.data_ptr(),
                   w.master.data_ptr() + 4 * w.offsets["embedding"], self.xs[0].data_ptr(), b, s)
         caches = []
+        # the blocks run as a chain: block l's residual down-projection also
+        # writes block l+1's normalised input h1 / inv1 (fused into one kernel
+        # at hidden 512) — into block l+1's full cache, or into a scratch pair
+        # for a lean block (the lean cache stays {x, x1})
+        structs = []
         for l in range(cfg.layers):
             full = None if mb.lean[l] else self._full_cache(l)
             cache = mdl.BlockCache(mode=mdl.CACHE_FFN_INPUT_ONLY if mb.lean[l] else mdl.CACHE_FULL,
                                    x=self.xs[l], x1=self.x1s[l], full=full)
             cs = cache.struct()
+            if mb.lean[l] and l > 0:  # lean h1 scratch (alternating: block l reads one, writes the other)
+                h1s, inv1s = self._h1_scratch(l % 2, b)
+                cs.h1, cs.inv1 = h1s.data_ptr(), inv1s.data_ptr()
+            structs.append(cs)
             caches.append(cs)
-            _lib.call("mecefo_forward_block", eng.handle, ctypes.byref(self.lws[l]), ctypes.byref(cs),
-                      self.xs[l + 1].data_ptr(), None, b,
-                      _lib.CACHE_FFN_INPUT_ONLY if mb.lean[l] else _lib.CACHE_FULL, ws, wn, s)
+        for l in range(cfg.layers):
+            cs = structs[l]
+            nxt = structs[l + 1] if l + 1 < cfg.layers else None
+            _lib.call("mecefo_forward_block_chained", eng.handle, ctypes.byref(self.lws[l]), ctypes.byref(cs),
+                      self.xs[l + 1].data_ptr(), b, _lib.CACHE_FFN_INPUT_ONLY if mb.lean[l] else _lib.CACHE_FULL,
+                      _lib.FWD_H1_READY if l > 0 else 0,
+                      w.get(f"layers.{l + 1}.norm_mha").data_ptr() if nxt is not None else None,
+                      nxt.h1 if nxt is not None else None, nxt.inv1 if nxt is not None else None, ws, wn, s)
         _lib.call("mecefo_head_forward_loss_grouped", eng.handle, self.xs[cfg.layers].data_ptr(),
                   w.get("final_norm").data_ptr(), w.shadow_view("unembedding").data_ptr(), self.tgt.data_ptr(), b, b1,
                   self.xf.data_ptr(), self.inv_f.data_ptr(), self.logits.data_ptr(), loss_ptr, ws, wn, s)

@@ -131,3 +131,49 @@ def test_forward_block_fused_residual_norm_at_bench_size(cuda):
     assert R.rel_err(y.cpu().numpy(), y_ref.reshape(x.shape)) < BF16_TOL
     y2, _ = mdl.forward_block(cfg, w.layers[0], xt, mdl.CACHE_FFN_INPUT_ONLY)
     assert torch.equal(y, y2)
+
+
+def test_chained_forward_matches_per_block_calls(cuda):
+    """mecefo_forward_block_chained (the step engine's forward: block l's down
+    projection also writes block l+1's h1 / inv1, fused into one kernel at
+    hidden 512 and 16384 tokens) against plain per-block calls, two lean
+    blocks: same outputs up to fp32 summation order / bf16 rounding ties."""
+    import ctypes
+
+    from paper_2510_16415_b200 import _lib, runtime
+
+    seqs = 64
+    cfg = mdl.ModelConfig(vocab=64, hidden=512, heads=8, ffn_intermediate=1376, layers=2, seq_len=256)
+    w = mdl.init_weights(cfg, 5, precision="bf16")
+    rng = np.random.Generator(np.random.PCG64(9))
+    x0 = torch.tensor(rng.normal(size=(seqs * 256, 512)) * 0.5, dtype=torch.float32, device="cuda")
+    eng = runtime.engine_for(cfg, "bf16")
+    b = x0.shape[0]
+    ws, wn = eng.workspace(b)
+    s = runtime.stream_ptr()
+    lean = _lib.CACHE_FFN_INPUT_ONLY
+
+    def run(chained):
+        xs = [x0.clone(), torch.empty_like(x0), torch.empty_like(x0)]
+        x1s = [torch.empty_like(x0) for _ in range(2)]
+        h1 = torch.empty(b, 512, dtype=torch.bfloat16, device="cuda")
+        inv1 = torch.empty(b, dtype=torch.float32, device="cuda")
+        for l in range(2):
+            cs = mdl.BlockCache(mode=mdl.CACHE_FFN_INPUT_ONLY, x=xs[l], x1=x1s[l]).struct()
+            if not chained:
+                _lib.call("mecefo_forward_block", eng.handle, ctypes.byref(w.layers[l].struct()), ctypes.byref(cs),
+                          xs[l + 1].data_ptr(), None, b, lean, ws, wn, s)
+                continue
+            if l == 1:
+                cs.h1, cs.inv1 = h1.data_ptr(), inv1.data_ptr()
+            gain = w.get("layers.1.norm_mha").data_ptr() if l == 0 else None
+            _lib.call("mecefo_forward_block_chained", eng.handle, ctypes.byref(w.layers[l].struct()),
+                      ctypes.byref(cs), xs[l + 1].data_ptr(), b, lean, _lib.FWD_H1_READY if l == 1 else 0, gain,
+                      h1.data_ptr() if l == 0 else None, inv1.data_ptr() if l == 0 else None, ws, wn, s)
+        torch.cuda.synchronize()
+        return xs, x1s
+
+    xs_a, x1s_a = run(False)
+    xs_b, x1s_b = run(True)
+    for t_a, t_b in ((x1s_a[0], x1s_b[0]), (xs_a[1], xs_b[1]), (x1s_a[1], x1s_b[1]), (xs_a[2], xs_b[2])):
+        assert R.rel_err(t_b.cpu().numpy(), t_a.cpu().numpy()) < 2e-3
