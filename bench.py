@@ -328,6 +328,15 @@ class Job:
 
             dist.barrier()
 
+    def min_over_ranks(self, v: int) -> int:
+        if self.group is None:
+            return v
+        import torch.distributed as dist
+
+        t = self.torch.tensor([float(min(v, 10**9))], device="cuda", dtype=self.torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return int(t.item())
+
     def max_over_ranks(self, v: float) -> float:
         if self.group is None:
             return v
@@ -341,8 +350,13 @@ class Job:
         """Run untimed steps past any projection refresh that would otherwise
         fall inside the next timed leg (refresh cost is measured separately,
         amortised over tau)."""
-        k = self.eng.steps_until_refresh(mbs)
-        if k <= steps + 1:
+        # collective: every step carries the Eq. (1) all-reduces, so all ranks
+        # run the same number of extra steps — until no rank's refresh falls
+        # inside the leg (a rank without lean layers never needs one)
+        for _ in range(4):  # (legs longer than tau cannot avoid a refresh: bounded)
+            k = self.min_over_ranks(self.eng.steps_until_refresh(mbs))
+            if k > steps + 1:
+                break
             for _ in range(k + 1):
                 self.eng.step(mbs, self.R, self.lr, skip=skip, check=False)
             self.torch.cuda.synchronize()
