@@ -380,18 +380,34 @@ class Job:
         n0 = self.lib.mecefo_launch_count()
         replays = 0
         t_wall = time.perf_counter()
+        # e2e: every step's losses are copied to pinned host memory and read by
+        # the host (two slots: the host reads step i-2's values while step i
+        # is queued, as a training loop logging its loss would; the last two
+        # are read after the final synchronize, inside the timed region)
+        if e2e:
+            hbuf = [torch.empty(self.R, dtype=torch.float32).pin_memory() for _ in range(2)]
+            hev = [torch.cuda.Event() for _ in range(2)]
+            self.e2e_losses = []
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st.record()
-        for _ in range(steps):
+        for i in range(steps):
             if graph and not self.eng.projections_due(mbs):
                 losses = self.eng.replay(self.lr, mbs, skip)
                 replays += 1
             else:
                 losses = self.eng.step(mbs, self.R, self.lr, skip=skip, check=False)
-            if e2e:
-                losses.cpu()  # D2H read of the step's result
+            if e2e:  # D2H read of the step's result
+                j = i % 2
+                if i >= 2:
+                    hev[j].synchronize()
+                    self.e2e_losses.append(hbuf[j].tolist())
+                hbuf[j].copy_(losses, non_blocking=True)
+                hev[j].record()
         en.record()
         torch.cuda.synchronize()
+        if e2e:
+            for i in range(max(0, steps - 2), steps):
+                self.e2e_losses.append(hbuf[i % 2].tolist())
         wall = time.perf_counter() - t_wall
         launches = self.lib.mecefo_launch_count() - n0 + replays * self.graph_launches.get(
             self.eng.plan_key(mbs, skip), 0)
@@ -822,6 +838,7 @@ def main():
         "drop_pct_instantaneous": round(100.0 * (1.0 - value_steady / ff_value), 2) if ff_value else None,
         "drop_pct_amortised": round(100.0 * (1.0 - value / ff_value), 2) if ff_value else None,
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "losses_read_per_rank": len(getattr(job, "e2e_losses", [])),
                 "d2h_bytes_per_step": 4 * R},
         "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
         "profiled_kernel_ms_per_step": round(kernel_ms / args.steps, 3),
