@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
   const int row0 = seq * a.T;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
   const uint32_t tmem = *tmem_holder;
 
   if (threadIdx.x == 0) {
-    mbar_expect_tx(&bars[0], 16384 + 2 * nk * 128);
+    // Q|K on bars[0] (S = Q K^T starts as soon as they land), V on bars[3] (needed by P V only)
+    mbar_expect_tx(&bars[0], 16384 + nk * 128);
+    mbar_expect_tx(&bars[3], nk * 128);
     tma_load_2d(sQ, &tq, &bars[0], h * 64, row0 + q0);
     tma_load_2d(sQ + 8192, &tq, &bars[0], h * 64, row0 + q0 + 64);
-    for (int kb = 0; kb < nk / 64; ++kb) {
-      tma_load_2d(sK + kb * 8192, &tq, &bars[0], a.m + h * 64, row0 + kb * 64);
-      tma_load_2d(sV + kb * 8192, &tq, &bars[0], 2 * a.m + h * 64, row0 + kb * 64);
-    }
+    for (int kb = 0; kb < nk / 64; ++kb) tma_load_2d(sK + kb * 8192, &tq, &bars[0], a.m + h * 64, row0 + kb * 64);
+    for (int kb = 0; kb < nk / 64; ++kb) tma_load_2d(sV + kb * 8192, &tq, &bars[3], 2 * a.m + h * 64, row0 + kb * 64);
     mbar_wait(&bars[0], 0);
     tc_fence_after();
     // S = Q K^T: A, B K-major; M = 128, N = nk, K = 64
@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int k0 = cb + cc + 2 * j;
-      const float p0 = (valid && k0 <= qi) ? exp2f((v[2 * j] - mx) * c2) : 0.f;
-      const float p1 = (valid && k0 + 1 <= qi) ? exp2f((v[2 * j + 1] - mx) * c2) : 0.f;
+      const float p0 = (valid && k0 <= qi) ? ex2_approx((v[2 * j] - mx) * c2) : 0.f;
+      const float p1 = (valid && k0 + 1 <= qi) ? ex2_approx((v[2 * j + 1] - mx) * c2) : 0.f;
       __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
       // the row sum uses the bf16-rounded probabilities that feed P V
       const float2 back = __bfloat1622float2(hp);
@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
   __syncthreads();
   l = red[256 + row] + red[384 + row];
   if (threadIdx.x == 0) {
+    mbar_wait(&bars[3], 0);
     tc_fence_after();
     // O = P V: A = P K-major (K = keys), B = V MN-major (N = d = 64)
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
