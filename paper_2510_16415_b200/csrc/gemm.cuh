@@ -491,6 +491,16 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
 #pragma unroll
     for (int j = 0; j < 16; ++j) o[j] = g[j] * e.alpha;
     if (e.rope_cos && n0 < e.rope_cols && row_ok) {
+      if (rope_pre && n0 + 16 <= e.rope_cols) {  // this row's (cos, sin) of these 8 frequencies, per tile
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float cs = rope_pre[j], sn = rope_pre[16 + j];
+          const float ev = o[2 * j], od = o[2 * j + 1];
+          o[2 * j] = ev * cs - od * sn;
+          o[2 * j + 1] = ev * sn + od * cs;
+        }
+        return;
+      }
       const int pos = r % e.rope_T, half = e.rope_hd >> 1;
       if ((e.rope_hd & 15) == 0 && n0 + 16 <= e.rope_cols) {
         // The 16-column span lies inside one head: 8 consecutive frequencies.
