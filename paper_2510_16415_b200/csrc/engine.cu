@@ -388,7 +388,10 @@ int dispatch_tc_major(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
 // Measured: pays off only for very large tile counts (the LM-head GEMMs,
 // +10%); neutral-to-negative on the per-layer GEMMs.
 bool use_cluster(const GemmCall& g, int BN) {
-  if (getenv("MECEFO_NO_CLUSTER") || g.b_diag_off) return false;  // the pair shares ONE B tile
+#ifdef MECEFO_TIMING_KNOBS
+  if (getenv("MECEFO_NO_CLUSTER")) return false;
+#endif
+  if (g.b_diag_off) return false;  // the pair shares ONE B tile
   const int64_t cpt = g.paired ? BN / 2 : BN;
   const int64_t tiles = ((g.M + 127) / 128) * ((g.N + cpt - 1) / cpt);
   // (paired gate|up GEMMs measured 9% slower clustered: excluded)
@@ -597,8 +600,12 @@ int rmsnorm_bwd(mecefo_engine* e, Ws& ws, const float* x, const float* g, const 
 // Which fused recompute kernel runs: 2 = the CTA-pair (cta_group::2) kernel,
 // 1 = the single-CTA kernel. MECEFO_DUAL=1 selects the latter.
 int dual_variant() {
+#ifdef MECEFO_TIMING_KNOBS
   static const int v = getenv("MECEFO_DUAL") ? atoi(getenv("MECEFO_DUAL")) : 2;
   return v == 1 ? 1 : 2;
+#else
+  return 2;
+#endif
 }
 
 // Fused d_act / gate / up tcgen05 kernel + SwiGLU backward epilogue (bf16).

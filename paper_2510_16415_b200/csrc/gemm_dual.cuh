@@ -552,8 +552,7 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
           stage_store32_db(stg, sb, &tmDg, g, n01, r0, lane);
           stage_store32_db(stg, sb, &tmDu, u, n01, r0, lane);
         }
-        continue;
-      }
+      } else {
 #pragma unroll 1
       for (int cc = 0; cc < CPW; ++cc) {
         const int c = cbase + cc;
@@ -589,6 +588,7 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
           }
         }
       }
+      }  // CPW != 2
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();

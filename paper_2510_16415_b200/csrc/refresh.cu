@@ -50,11 +50,13 @@ constexpr int kSlots = 96;  // device job-array slots per outer iteration
 // clamp(kChebScale / residual, kChebMin, kChebMax); overridable for experiments
 // through MECEFO_CHEB="min,max,scale".
 double kChebMin = 1e8, kChebMax = 1e12, kChebScale = 1e4;
+#ifdef MECEFO_TIMING_KNOBS  // experiments only (libmecefo_timing.so)
 struct ChebEnv {
   ChebEnv() {
     if (const char* v = getenv("MECEFO_CHEB")) sscanf(v, "%lf,%lf,%lf", &kChebMin, &kChebMax, &kChebScale);
   }
 } g_cheb_env;
+#endif
 constexpr size_t kSmemLimit = 227 * 1024;
 
 struct RfPlan {
@@ -499,7 +501,6 @@ int mecefo_refresh_converged(mecefo_engine* e, mecefo_refresh_job* jobs, int32_t
       for (int i : fin_jobs) {
         RfPlan& p = plans[i];
         const mecefo_refresh_job& jb = jobs[i];
-        double* th = cx.summary + (size_t)i * (kmax + 2);
         if (!p.dual) {
           cj.push_back(CopyJob{jb.v1, p.V, p.r, p.k, jb.v1_f64, nullptr, (int)p.n, p.r, 0});
           continue;

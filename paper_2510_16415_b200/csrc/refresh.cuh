@@ -187,7 +187,6 @@ constexpr int RF_SMALL_THREADS = 1024;
 // of a warp hit distinct banks).
 __global__ void __launch_bounds__(RF_SMALL_THREADS) cholqr_kernel(const SmallJob* __restrict__ jobs) {
   extern __shared__ double rf_smem[];
-  __shared__ double red[32];
   const SmallJob jb = jobs[blockIdx.x];
   const int k = jb.k, ld = k | 1, tid = threadIdx.x, nt = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;

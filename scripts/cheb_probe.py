@@ -1,5 +1,6 @@
 """Converged refresh under one Chebyshev amplification setting (MECEFO_CHEB,
-read at library load): wall time, products, RR steps, residuals, and the
+read at library load by the timing build: run with
+MECEFO_LIB=paper_2510_16415_b200/libmecefo_timing.so): wall time, products, RR steps, residuals, and the
 projector distance of the bases to a reference solve saved by the first run
 (/tmp/cheb_ref_<model>.pt)."""
 import json, os, sys, time, torch
