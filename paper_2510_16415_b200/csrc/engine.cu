@@ -262,7 +262,8 @@ Epilogue epi_store(void* out, int64_t ldo, int out_prec, float alpha = 1.f, floa
 
 template <int BN, bool AK, bool BKM, int CL, int NG, bool ROPE = false>
 int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
-  using C = TcCfg<BN>;
+  constexpr int CLN = CL == CL_2SM ? 2 : CL;  // CTAs per cluster
+  using C = TcCfg<BN, CL == CL_2SM>;
   static_assert(NG == 1 || CL == 1, "grouped launches are single-CTA");
   const int ng = NG > 1 ? g.groups : 1;
   if (ng < 1 || ng > NG) return set_err(MECEFO_ERR_CONSISTENCY, "group count %d outside [1, %d]", ng, NG);
@@ -292,7 +293,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   const int cols_per_tile = g.paired ? BN / 2 : BN;
   p.tiles_n = (int)((g.N + cols_per_tile - 1) / cols_per_tile);
   p.num_tiles = p.tiles_m * p.tiles_n * p.split * ng;
-  p.tiles_m_cl = (p.tiles_m + CL - 1) / CL;
+  p.tiles_m_cl = (p.tiles_m + CLN - 1) / CLN;
   p.split_tiles = p.tiles_m_cl * p.tiles_n * p.split;
   p.num_tiles_cl = p.split_tiles * ng;
   // A-heavy GEMMs with few N tiles (d_h2, the residual GEMMs, head d_xf): N-fastest
@@ -352,8 +353,8 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
 #endif
   auto kern = gemm_tc_kernel<BN, AK, BKM, CL, NG, ROPE>;
   TRY(ensure_smem((const void*)kern, C::SMEM));
-  const int grid = CL * std::min(p.num_tiles_cl, kNumSMs / CL);
-  if (CL == 1) {
+  const int grid = CLN * std::min(p.num_tiles_cl, kNumSMs / CLN);
+  if (CLN == 1) {
     CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(TC_THREADS), C::SMEM, s, mp, p, outs));
     return check_launch("gemm_tc_kernel");
   }
@@ -364,7 +365,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.x = CLN;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -400,6 +401,24 @@ bool use_cluster(const GemmCall& g, int BN) {
   if (const char* v = getenv("MECEFO_CLUSTER_MIN_TILES")) min_tiles = atoll(v);
 #endif
   return BN >= 128 && !g.paired && (g.M + 127) / 128 >= 2 && tiles >= min_tiles;
+}
+
+// CTA pairs with ONE cta_group::2 MMA (M = 256 per pair, each CTA stages its
+// A rows and half of the B tile): BN = 256 single-group GEMMs with at least
+// two M tiles and a long K. Halves the B bytes each CTA moves through shared
+// memory, the operand-bandwidth limit of long 128 x 256 mainloops. Measured
+// (C1, 16384 tokens): head g_unemb (K 16384) +9 %, d_xf (K 32000) +6 %,
+// d_h2 (K 2752) +4 %, exact wgrad_gu +8 %; the K = 512 GEMMs with heavy epilogues (logits, QKV +
+// RoPE, gate|up + SwiGLU) lost 5-10 % (shorter tiles: the pair's shared
+// accumulator hand-off exposes more of the epilogue), so they stay single.
+bool use_2sm(const GemmCall& g, int BN) {
+  int64_t min_k = 1024;
+#ifdef MECEFO_TIMING_KNOBS
+  if (getenv("MECEFO_NO_2SM")) return false;
+  if (const char* v = getenv("MECEFO_2SM_MIN_K")) min_k = atoll(v);
+#endif
+  // (fp32 residual epilogues excluded: down_residual, K 1376, lost 6 %)
+  return BN == 256 && !g.b_diag_off && (g.M + 127) / 128 >= 2 && g.K >= min_k && !g.epi.residual;
 }
 
 // Tile width for the tcgen05 path. The MMA time of a tile is proportional to
@@ -464,8 +483,11 @@ int run_gemm(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   if (e->prec == PREC_BF16) {
     if (g.paired && !g.b.km) return set_err(MECEFO_ERR_CONSISTENCY, "paired GEMM needs a K-major B");
     const int BN = choose_bn(g);
-    if (g.epi.rope_cos && BN == 256 && g.a.km && g.b.km && !g.paired && !use_cluster(g, BN))
-      return launch_tc<256, true, true, 1, 1, true>(e, g, s);  // QKV with RoPE (per-tile angle table)
+    const bool two = use_2sm(g, BN);
+    if (g.epi.rope_cos && BN == 256 && g.a.km && g.b.km && !g.paired && (two || !use_cluster(g, BN)))
+      return two ? launch_tc<256, true, true, CL_2SM, 1, true>(e, g, s)  // QKV with RoPE (per-tile angle table)
+                 : launch_tc<256, true, true, 1, 1, true>(e, g, s);
+    if (two) return dispatch_tc_major<256, CL_2SM>(e, g, s);
     const bool cl = use_cluster(g, BN);
     if (BN == 256) return cl ? dispatch_tc_major<256, 2>(e, g, s) : dispatch_tc_major<256, 1>(e, g, s);
     if (BN == 128) return cl ? dispatch_tc_major<128, 2>(e, g, s) : dispatch_tc_major<128, 1>(e, g, s);

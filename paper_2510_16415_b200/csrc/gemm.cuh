@@ -335,6 +335,45 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t tmem_d, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// CTA-pair (cta_group::2) primitives: one MMA over M = 256 rows, A rows and
+// half of B staged in each CTA of the pair.
+__device__ __forceinline__ void tc_mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the LEADER's barrier
+// (the cta-rank bit of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
@@ -382,12 +421,20 @@ constexpr int TC_EPI_WARPS = 8;                        // 2 per TMEM lane quadra
 constexpr int TC_THREADS = 128 + 32 * TC_EPI_WARPS;    // warps 0-3: TMA, MMA, TMEM alloc, spare
 constexpr int TC_STAGE_OUT = 4096;                     // per-epilogue-warp staging: 32 rows x 128 B
 
-template <int BN>
+// CL template value of a CTA pair running ONE cta_group::2 MMA per k-step:
+// M = 256 rows per pair tile (128 per CTA, each in its own TMEM), each CTA
+// stages its own A rows and HALF of the B tile, so a CTA's operand traffic
+// through shared memory per flop drops by a quarter at BN = 256 (A 16 KB +
+// B 16 KB per 64-deep k-block instead of 16 + 32 KB) and the ring holds six
+// stages instead of four.
+constexpr int CL_2SM = 3;
+
+template <int BN, bool TWO = false>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int B_BYTES = (TWO ? BN / 2 : BN) * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = TWO ? 6 : ((BN == 256) ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int EPI_BYTES = TC_EPI_WARPS * TC_STAGE_OUT;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
@@ -595,7 +642,10 @@ __device__ __forceinline__ void epi_slot16(const Epilogue& e, int slot, int r, i
 template <int BN, bool A_KMAJOR, bool B_KMAJOR, int CL, int NG, bool ROPE = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ TcMaps<NG> mp, GemmDev p, TcOut outs) {
-  using C = TcCfg<BN>;
+  constexpr bool TWO = CL == CL_2SM;  // CTA pair, cta_group::2 MMA issued by the leader
+  constexpr int CLN = TWO ? 2 : CL;   // CTAs per cluster
+  static_assert(!TWO || BN == 256, "the pair mode stages B halves of 128 rows");
+  using C = TcCfg<BN, TWO>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -623,29 +673,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], TWO ? 1 : CL);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 32 * TC_EPI_WARPS);
+      mbar_init(&tempty[s], TWO ? 2 * TC_EPI_WARPS : 32 * TC_EPI_WARPS);  // pair: one arrive per warp of both CTAs
     }
     for (int w = 0; w < 2 * TC_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.a[0])) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.b[0])) : "memory");
   }
-  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
-  const int cl_id = blockIdx.x / CL, n_cl = gridDim.x / CL;
-  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
+  const int crank = CLN > 1 ? (int)cluster_ctarank() : 0;
+  const int cl_id = blockIdx.x / CLN, n_cl = gridDim.x / CLN;
+  constexpr uint16_t kMask = (uint16_t)((1u << CLN) - 1);
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"((uint32_t)C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (TWO) {  // the pair's TMEM, allocated by the same warp of both CTAs
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
+  if (CLN > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
   griddep_wait();  // predecessor outputs are visible from here on
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
@@ -657,7 +714,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
         int mt, nt, ks, grp;
-        decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
+        decode_tile_cl(p, t, crank, CLN, mt, nt, ks, grp);
         const CUtensorMap* tmA = &mp.a[NG > 1 ? grp : 0];
         const CUtensorMap* tmB = &mp.b[NG > 1 ? grp : 0];
         // once per tile: this single thread issues every TMA of the k-loop, so
@@ -667,10 +724,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
+          if constexpr (TWO) {
+            // both CTAs' bytes complete on the LEADER's barrier (its MMA reads both)
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if (A_KMAJOR) {
+              tma_load_2d_2sm(a, tmA, &full[stage], k0, mt * TC_BM);
+            } else {
+              tma_load_2d_2sm(a, tmA, &full[stage], mt * TC_BM, k0);
+              tma_load_2d_2sm(a + 8192, tmA, &full[stage], mt * TC_BM + 64, k0);
+            }
+            if (B_KMAJOR) {  // rows [crank * BN/2, +BN/2) of the tile (paired: CTA 0 gate, CTA 1 up)
+              const int row = p.paired ? (crank == 0 ? nt * (BN / 2) : nt * (BN / 2) + (int)p.pair_off)
+                                       : nt * BN + crank * (BN / 2);
+              tma_load_2d_2sm(b, tmB, &full[stage], k0, row);
+            } else {         // 64-column chunks [crank * NCH/2, +NCH/2) of the tile
+              constexpr int NCH = BN / 64;
+#pragma unroll
+              for (int c = 0; c < NCH / 2; ++c) {
+                const int cc = crank * (NCH / 2) + c;
+                const int col = !p.paired ? nt * BN + cc * 64
+                                          : (cc < NCH / 2 ? nt * (BN / 2) + cc * 64
+                                                          : nt * (BN / 2) + (int)p.pair_off + (cc - NCH / 2) * 64);
+                tma_load_2d_2sm(b + c * 8192, tmB, &full[stage], col, k0);
+              }
+            }
+            if (++stage == nst) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           if (A_KMAJOR) {
             tma_load_2d(a, tmA, &full[stage], k0, mt * TC_BM);
           } else {
@@ -709,18 +793,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (single thread) =====
+    if (lane == 0 && (!TWO || crank == 0)) {
+      // ===== MMA issuer (single thread; the pair's leader in TWO mode) =====
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
                                  ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                                 ((uint32_t)(TC_BM >> 4) << 24);
+                                 ((uint32_t)((TWO ? 2 * TC_BM : TC_BM) >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
         int mt, nt, ks, grp;
-        decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
+        decode_tile_cl(p, t, crank, CLN, mt, nt, ks, grp);
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.kblocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -735,15 +819,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < TC_BK / 16; ++k) {
             const uint64_t ad = A_KMAJOR ? make_sdesc(a_addr + k * 32, 16, 1024) : make_sdesc(a_addr + k * 2048, 8192, 1024);
             const uint64_t bd = B_KMAJOR ? make_sdesc(b_addr + k * 32, 16, 1024) : make_sdesc(b_addr + k * 2048, 8192, 1024);
-            tc_mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if constexpr (TWO)
+              tc_mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else
+              tc_mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          if (CL > 1)
+          if (TWO)
+            tc_commit_2sm_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
+          else if (CL > 1)
             tc_commit_mc(&empty[stage], kMask);  // the stage holds the peer's multicast half too
           else
             tc_commit(&empty[stage]);
           if (++stage == nst) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        if (TWO)
+          tc_commit_2sm_mc(&tfull[acc], 0x3);  // both CTAs' accumulators are ready
+        else
+          tc_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -772,7 +864,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int NCHUNK_PAIR = BN / 64;
     for (int t = cl_id; t < p.num_tiles_cl; t += n_cl) {
       int mt, nt, ks, grp;
-      decode_tile_cl(p, t, crank, CL, mt, nt, ks, grp);
+      decode_tile_cl(p, t, crank, CLN, mt, nt, ks, grp);
       const CUtensorMap* tmO0 = &mp.o0[NG > 1 ? grp : 0];
       const int r0 = mt * TC_BM + quad * 32;
       const int nchunks = p.paired ? NCHUNK_PAIR : NCHUNK_PLAIN;
@@ -840,7 +932,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // this warp's last chunk is in registers: hand the accumulator
           // back to the MMA warp before the math and stores
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          if constexpr (TWO) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
+          } else {
+            mbar_arrive(&tempty[acc]);
+          }
           released = true;
         }
 #pragma unroll
@@ -889,7 +986,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (!released) {
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if constexpr (TWO) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -898,11 +1000,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
+  if (CLN > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it / signal it
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)C::TMEM_COLS)
-                 : "memory");
+    if constexpr (TWO)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
   }
 }
 

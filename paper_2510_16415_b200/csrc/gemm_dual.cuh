@@ -67,12 +67,18 @@ __device__ __forceinline__ void store_row32_bf16(__nv_bfloat16* p, const float* 
   }
 }
 
-// SwiGLU backward of one element (model.py:198-204, 216, 250-253), ~11
-// instructions: s = sigmoid(g) by MUFU ex2 + rcp.approx, gs = silu(g),
+// SwiGLU backward of one element (model.py:198-204, 216, 250-253), ~10
+// instructions: s = sigmoid(g) = (1 + tanh(g/2)) / 2 by ONE MUFU op
+// (tanh.approx, |error| <= 2^-11 relative to tanh, i.e. <= 2.5e-4 absolute
+// in s, an eighth of a bf16 ulp at s ~ 0.5; these outputs are bf16), gs = silu(g),
 //   act = gs u,  d_up = d gs,  d_gate = d u s (1 + g (1 - s)) = d u (s + gs - gs s).
 // In: g = gate, u = up, d = d_act; out: g = d_gate, u = d_up, d = act.
 __device__ __forceinline__ void swiglu_bwd_elem(float& g, float& u, float& d) {
+#ifdef MECEFO_TIMING_KNOBS  // timing build: the two-MUFU form, for A/B against the product's one-MUFU form
   const float s = rcp_approx(1.f + ex2_approx(-1.4426950408889634f * g));
+#else
+  const float s = sigmoid_tanh(g);
+#endif
   const float gs = g * s;
   const float du = d * gs;
   const float dg = (d * u) * (s + fmaf(-gs, s, gs));
@@ -334,43 +340,6 @@ struct D2S {
   static constexpr int THREADS = 128 + 32 * EPW;
   static constexpr int SMEM = STAGES * D2S_STAGE_BYTES + EPW * TC_STAGE_OUT + 1024 + 256;
 };
-
-__device__ __forceinline__ void tc_mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                                uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   smem_u32(bar)),
-               "h"(mask)
-               : "memory");
-}
-// TMA into this CTA's smem, completion bytes counted on the LEADER's barrier
-// (the cta-rank bit of the shared::cluster address cleared).
-__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
-  asm volatile(
-      "{\n"
-      ".reg .b32 ra;\n"
-      "mapa.shared::cluster.u32 ra, %0, %1;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(cta)
-      : "memory");
-}
 
 template <int EPW>
 __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)

@@ -12,8 +12,12 @@ from paper_2510_16415_b200 import _lib, runtime
 
 pytestmark = pytest.mark.gpu
 
+# (4696, 1000, 1096) takes BN = 256 and (K >= 1024) the CTA-pair
+# cta_group::2 path, with an odd M-tile count (the last pair's
+# second CTA has no rows), a ragged last N tile and a partial k-block;
+# (8192, 512, 512) the single-CTA BN = 256 path
 SHAPES = [(128, 64, 64), (256, 256, 128), (296, 200, 104), (1000, 768, 520), (64, 16, 16), (8192, 512, 512),
-          (512, 128, 8192)]
+          (512, 128, 8192), (4696, 1000, 1096)]
 
 
 def _engine(precision):
