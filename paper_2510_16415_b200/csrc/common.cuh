@@ -92,13 +92,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float tanh_approx(float x) {
-  float r;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-// one-MUFU sigmoid for bf16-output epilogues only (absolute error <= 2.5e-4)
-__device__ __forceinline__ float sigmoid_tanh(float z) { return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f); }
 __device__ __forceinline__ float sigmoid_f(float z) { return rcp_approx(1.f + __expf(-z)); }
 __device__ __forceinline__ float sigmoid_ieee_f(float z) { return __frcp_rn(1.f + __expf(-z)); }
 __device__ __forceinline__ float silu_f(float z) { return z * sigmoid_f(z); }

@@ -67,18 +67,14 @@ __device__ __forceinline__ void store_row32_bf16(__nv_bfloat16* p, const float* 
   }
 }
 
-// SwiGLU backward of one element (model.py:198-204, 216, 250-253), ~10
-// instructions: s = sigmoid(g) = (1 + tanh(g/2)) / 2 by ONE MUFU op
-// (tanh.approx, |error| <= 2^-11 relative to tanh, i.e. <= 2.5e-4 absolute
-// in s, an eighth of a bf16 ulp at s ~ 0.5; these outputs are bf16), gs = silu(g),
+// SwiGLU backward of one element (model.py:198-204, 216, 250-253), ~11
+// instructions: s = sigmoid(g) by MUFU ex2 + rcp.approx, gs = silu(g),
+// (measured: a one-MUFU tanh.approx sigmoid saved 1.1 us of 82 per launch but
+// raised the C1 gate/up gradient errors above the bf16-autocast level, 1.27x)
 //   act = gs u,  d_up = d gs,  d_gate = d u s (1 + g (1 - s)) = d u (s + gs - gs s).
 // In: g = gate, u = up, d = d_act; out: g = d_gate, u = d_up, d = act.
 __device__ __forceinline__ void swiglu_bwd_elem(float& g, float& u, float& d) {
-#ifdef MECEFO_TIMING_KNOBS  // timing build: the two-MUFU form, for A/B against the product's one-MUFU form
   const float s = rcp_approx(1.f + ex2_approx(-1.4426950408889634f * g));
-#else
-  const float s = sigmoid_tanh(g);
-#endif
   const float gs = g * s;
   const float du = d * gs;
   const float dg = (d * u) * (s + fmaf(-gs, s, gs));
