@@ -269,6 +269,10 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   if (ng < 1 || ng > NG) return set_err(MECEFO_ERR_CONSISTENCY, "group count %d outside [1, %d]", ng, NG);
   TcMaps<NG> mp;
   std::memset(&mp, 0, sizeof(mp));
+  bool b_split = false;
+#ifdef MECEFO_TIMING_KNOBS
+  b_split = BN == 256 && BKM && CL == 1 && !g.paired && getenv("MECEFO_B_SPLIT") != nullptr;
+#endif
   const int64_t rowsB =
       g.paired ? g.pair_off + g.N : g.N + g.b_diag_off * (((g.M + TC_BM - 1) / TC_BM - 1) / std::max(1, g.b_diag_div));
   for (int q = 0; q < ng; ++q) {
@@ -276,7 +280,7 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
     const void* pb = NG > 1 ? g.gb[q] : g.b.p;
     if (AK) TRY(make_tmap(e, &mp.a[q], pa, g.K, g.M, g.a.ld, 64, TC_BM));
     else TRY(make_tmap(e, &mp.a[q], pa, g.M, g.K, g.a.ld, 64, 64));
-    if (BKM) TRY(make_tmap(e, &mp.b[q], pb, g.K, rowsB, g.b.ld, 64, (g.paired || CL > 1) ? BN / 2 : BN));
+    if (BKM) TRY(make_tmap(e, &mp.b[q], pb, g.K, rowsB, g.b.ld, 64, (g.paired || CL > 1 || b_split) ? BN / 2 : BN));
     else TRY(make_tmap(e, &mp.b[q], pb, rowsB, g.K, g.b.ld, 64, 64));
   }
   GemmDev p{};
@@ -300,6 +304,13 @@ int launch_tc(mecefo_engine* e, const GemmCall& g, cudaStream_t s) {
   // order so an A row block is streamed from HBM once (measured: d_h2 read
   // 159 MB for a 90 MB A with the M-fastest order)
   p.n_fast = (p.tiles_n >= 2 && p.tiles_n <= 8 && (double)g.M >= 4.0 * (double)g.N * (g.paired ? 2 : 1)) ? 1 : 0;
+  p.b_split = b_split ? 1 : 0;
+#ifdef MECEFO_TIMING_KNOBS
+  if (const char* v = getenv("MECEFO_NFAST_FOR")) {  // "tag=0|1,..."
+    const char* hit = g.tag ? strstr(v, g.tag) : nullptr;
+    if (hit && hit[strlen(g.tag)] == '=') p.n_fast = atoi(hit + strlen(g.tag) + 1);
+  }
+#endif
   p.epi = g.epi;
   // output slots -> TMA store / reduce-add maps (32 x 32 boxes, swizzled)
   TcOut outs{};

@@ -66,6 +66,7 @@ struct GemmDev {
   int tiles_m_cl, num_tiles_cl;  // tiles in units of CTA clusters along M (CL = 1 or 2); x groups
   int split_tiles;               // tiles_m_cl * tiles_n * split (one group)
   int n_fast;                    // tile order: N fastest (A-heavy GEMMs: the N tiles of an A row block run together)
+  int b_split;                   // K-major B (single CTA, unpaired) loaded as two BN/2-row boxes
   Epilogue epi;
 };
 
@@ -766,6 +767,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const int row = p.paired ? (crank == 0 ? nt * (BN / 2) : nt * (BN / 2) + (int)p.pair_off)
                                        : nt * BN + crank * (BN / 2);
               tma_load_2d_mc(b + crank * (BN / 2) * 128, tmB, &full[stage], k0, row, kMask);
+            } else if (!p.paired && p.b_split) {
+              tma_load_2d(b, tmB, &full[stage], k0, nt * BN + boff);
+              tma_load_2d(b + (BN / 2) * 128, tmB, &full[stage], k0, nt * BN + boff + BN / 2);
             } else if (!p.paired) {
               tma_load_2d(b, tmB, &full[stage], k0, nt * BN + boff);
             } else {
