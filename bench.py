@@ -207,7 +207,7 @@ def run_reference(args, rank: int, dims: dict):
                             "sample": f"{'faultsim.harness._rank_pass' if ref.kind == 'reference' else 'oracle port'}"
                                       f", all layers lean, {ref.seqs} seq/step", "host": host_info()},
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # --------------------------------------------------------------------------
@@ -603,8 +603,27 @@ def run_scenario(args, dims, world, rank, local, group):
                "refreshes": [{"iteration": a_, "matrices": b_, "products_max": c_, "fused": d_, "solve_ms": e_}
                              for a_, b_, c_, d_, e_ in refresh_log[:32]], "iteration_breakdown": breakdown,
                "events": events_log[:64]}
-        print(json.dumps(out), flush=True)
+        emit(out)
     _finish(group, job.eng)
+
+
+_JSON_OUT = None
+
+
+def _stdout_to_stderr():
+    """Route everything written to fd 1 (library banners such as NCCL's
+    version line) to stderr; the JSON line still goes to the real stdout."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(obj):
+    """The one JSON line of this run, on the real stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
 
 
 def main():
@@ -650,6 +669,8 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if world > 1:
+        _stdout_to_stderr()  # NCCL's own banner lines must not precede the JSON line
     torch.cuda.set_device(local)
     group = None
     if world > 1:
@@ -677,7 +698,7 @@ def main():
         ms, _, _ = job.timed(degraded, skip_d, args.steps)
         torch.cuda.cudart().cudaProfilerStop()
         if rank == 0:
-            print(json.dumps({"profile_only": True, "ms_per_step": ms / args.steps}), flush=True)
+            emit({"profile_only": True, "ms_per_step": ms / args.steps})
         return
 
     # value: CUDA-graph replay of the degraded iteration, inputs resident in HBM
@@ -848,7 +869,7 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clk.summary(), "loss_finite": loss_ok, "wall_s_timed": round(wall, 3),
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
     _finish(group, eng)
 
 
