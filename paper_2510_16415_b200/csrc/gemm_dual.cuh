@@ -337,6 +337,52 @@ struct D2S {
   static constexpr int SMEM = STAGES * D2S_STAGE_BYTES + EPW * TC_STAGE_OUT + 1024 + 256;
 };
 
+// Release-first epilogue helpers (swiglu_bwd_dual2sm_kernel<8>): a chunk's
+// d_act / gate / up (32 columns of one TMEM lane row each) read 8 columns at
+// a time and kept as bf16 pairs; then, after the tile's TMEM is released,
+// the SwiGLU backward in place and the three staged bf16 stores.
+__device__ __forceinline__ void dual_load_chunk_bf16(uint32_t lanes, uint32_t dcol, int c, uint32_t (&w)[48]) {
+  const uint32_t gcol = (uint32_t)((c >> 1) * 128 + (c & 1) * 32), ucol = gcol + 64u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // 8 columns at a time: 24 fp32 registers in flight
+    float d[8], g[8], u[8];
+    tmem_ld8_nowait(lanes + dcol + c * 32 + q * 8, d);
+    tmem_ld8_nowait(lanes + gcol + q * 8, g);
+    tmem_ld8_nowait(lanes + ucol + q * 8, u);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 a2 = __floats2bfloat162_rn(d[2 * j], d[2 * j + 1]);
+      __nv_bfloat162 g2 = __floats2bfloat162_rn(g[2 * j], g[2 * j + 1]);
+      __nv_bfloat162 u2 = __floats2bfloat162_rn(u[2 * j], u[2 * j + 1]);
+      w[q * 4 + j] = *reinterpret_cast<uint32_t*>(&a2);
+      w[16 + q * 4 + j] = *reinterpret_cast<uint32_t*>(&g2);
+      w[32 + q * 4 + j] = *reinterpret_cast<uint32_t*>(&u2);
+    }
+  }
+}
+__device__ __forceinline__ void dual_finish_chunk(uint32_t (&w)[48], uint8_t* stg, int& sb, const CUtensorMap* tmAct,
+                                                  const CUtensorMap* tmDg, const CUtensorMap* tmDu, int has_act,
+                                                  int n0, int r0, int lane) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {  // word j of d / g / u -> act / d_gate / d_up
+    // bf16 -> fp32 by bit placement (no address taken: w stays in registers)
+    float d0 = __uint_as_float(w[j] << 16), d1 = __uint_as_float(w[j] & 0xffff0000u);
+    float g0 = __uint_as_float(w[16 + j] << 16), g1 = __uint_as_float(w[16 + j] & 0xffff0000u);
+    float u0 = __uint_as_float(w[32 + j] << 16), u1 = __uint_as_float(w[32 + j] & 0xffff0000u);
+    swiglu_bwd_elem(g0, u0, d0);
+    swiglu_bwd_elem(g1, u1, d1);
+    __nv_bfloat162 a2 = __floats2bfloat162_rn(d0, d1), g2 = __floats2bfloat162_rn(g0, g1),
+                   u2 = __floats2bfloat162_rn(u0, u1);
+    w[j] = *reinterpret_cast<uint32_t*>(&a2);
+    w[16 + j] = *reinterpret_cast<uint32_t*>(&g2);
+    w[32 + j] = *reinterpret_cast<uint32_t*>(&u2);
+  }
+  if (has_act) stage_store32_db_packed(stg, sb, tmAct, w, n0, r0, lane);
+  stage_store32_db_packed(stg, sb, tmDg, w + 16, n0, r0, lane);
+  stage_store32_db_packed(stg, sb, tmDu, w + 32, n0, r0, lane);
+}
+
 template <int EPW>
 __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
     swiglu_bwd_dual2sm_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmH2,
@@ -461,6 +507,23 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
       const int r0 = mt * 2 * TC_BM + (int)crank * TC_BM + quad * 32;
       const uint32_t lanes = tmem_base + ((uint32_t)(quad * 32) << 16);
       if constexpr (CPW == 2) {
+#ifndef MECEFO_TIMING_KNOBS
+        // Release-first: both chunks' d_act / gate / up are read from TMEM and
+        // kept as bf16 pairs (48 words per chunk: the bf16 values a bf16
+        // autocast step would hold for these GEMM outputs), the tile's TMEM
+        // goes back to the leader's MMA right after the second read, and the
+        // SwiGLU backward math and the six staged stores run off the
+        // critical path, overlapping the next tile's gate|up product.
+        uint32_t w0[48], w1[48];  // per chunk: d words 0-15 | g 16-31 | u 32-47
+        dual_load_chunk_bf16(lanes, dcol, cbase, w0);
+        dual_load_chunk_bf16(lanes, dcol, cbase + 1, w1);
+        tc_fence_before();  // this warp's TMEM reads of the tile are done: release to the leader's MMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(edone, 0);
+        const int n00 = nt * D2_NP + cbase * 32, n01 = n00 + 32;
+        if (n00 < p.NP && r0 < p.M) dual_finish_chunk(w0, stg, sb, &tmAct, &tmDg, &tmDu, p.has_act, n00, r0, lane);
+        if (n01 < p.NP && r0 < p.M) dual_finish_chunk(w1, stg, sb, &tmAct, &tmDg, &tmDu, p.has_act, n01, r0, lane);
+#else
         // Early release: chunk 0 is loaded, computed and kept PACKED (48
         // words) while chunk 1 is loaded; the tile's TMEM is released right
         // after that second load — before any store — so the next tile's
@@ -517,6 +580,7 @@ __global__ void __launch_bounds__(D2S<EPW>::THREADS, 1)
           stage_store32_db(stg, sb, &tmDg, g, n01, r0, lane);
           stage_store32_db(stg, sb, &tmDu, u, n01, r0, lane);
         }
+#endif
       } else {
 #pragma unroll 1
       for (int cc = 0; cc < CPW; ++cc) {
