@@ -1,5 +1,6 @@
 # One measurement pass on a B200: GPU parity suite, smoke, the default bench
-# line, and the ncu launch list of one timed degraded step. Outputs under gpurun_out/final/.
+# line, the reference arm, the ncu launch list of one timed degraded step and
+# an ncu --set full of the dominant kernel. Outputs under gpurun_out/final/.
 set -x
 export PYTHONPATH=$PWD
 mkdir -p gpurun_out/final
@@ -10,3 +11,8 @@ timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/f
 python bench.py --profile-only --steps 1 --warmup 3 > gpurun_out/final/plain_profile_only.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
     --log-file gpurun_out/final/launches.csv python bench.py --profile-only --steps 1 --warmup 3 > gpurun_out/final/ncu_launch.log 2>&1
+python scripts/fwd_probe.py > gpurun_out/final/fwd_plain.txt 2>&1 && \
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k "regex:swiglu_bwd_dual2sm" -s 2 -c 1 -o /tmp/dual python scripts/fwd_probe.py > gpurun_out/final/ncu_dual.log 2>&1
+ncu -i /tmp/dual.ncu-rep --page raw --csv > gpurun_out/final/dual_raw.csv 2>&1
+ncu -i /tmp/dual.ncu-rep --page details --csv > gpurun_out/final/dual_details.csv 2>&1
